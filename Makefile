@@ -1,0 +1,42 @@
+# Build recipe for the B200 fused-LCE operator, its C oracle and the
+# reference-built checker.  `python -c "import __graft_entry__ as g; g.build()"`
+# runs the same targets.
+NVCC      ?= nvcc
+CXX       ?= g++
+CC        ?= gcc
+ARCH      := -gencode arch=compute_100a,code=sm_100a
+NVFLAGS   := $(ARCH) -O3 -lineinfo -std=c++17 -Xcompiler -fPIC -Xcompiler -Wall \
+             --expt-relaxed-constexpr -diag-suppress 177
+REF_DIR   ?= /root/reference/proj
+
+PKG       := paper_2511_17599_b200
+CSRC      := $(PKG)/csrc
+LIB       := $(PKG)/libfce.so
+ORACLE    := oracle/liboracle.so
+REF_LIB   := oracle/_ref/libfce_ref.so
+
+all: $(LIB) $(ORACLE) ref
+
+$(LIB): $(CSRC)/fce_kernels.cu $(CSRC)/fce_api.cpp $(CSRC)/fce_vp.cpp $(CSRC)/fce_internal.h \
+        $(CSRC)/sm100_ptx.cuh include/fce/fce.h
+	$(NVCC) $(NVFLAGS) -shared -cudart static -o $@ $(CSRC)/fce_kernels.cu $(CSRC)/fce_api.cpp \
+	    $(CSRC)/fce_vp.cpp -ldl -lpthread -lrt
+
+$(ORACLE): oracle/fce_oracle.c oracle/fce_oracle.h
+	$(CC) -O2 -std=c11 -fPIC -shared -fopenmp -ffp-contract=off -o $@ oracle/fce_oracle.c -lm
+
+# The reference itself, compiled in place from /root/reference (header-only
+# C++20) through a thin extern "C" shim; output stays in oracle/_ref/.
+ref:
+	@if [ -d "$(REF_DIR)/include/fusedce" ]; then $(MAKE) $(REF_LIB); \
+	 else echo "reference tree absent: using prebuilt $(REF_LIB) if present"; fi
+
+$(REF_LIB): oracle/ref_shim.cpp
+	mkdir -p oracle/_ref
+	$(CXX) -std=c++20 -O3 -march=x86-64-v3 -fPIC -shared -pthread -Dfusedce=fusedce_ref \
+	    -I$(REF_DIR)/include -o $@ oracle/ref_shim.cpp
+
+clean:
+	rm -f $(LIB) $(ORACLE) $(REF_LIB)
+
+.PHONY: all ref clean

@@ -1,0 +1,622 @@
+// C-ABI implementation (include/fce/fce.h): argument validation with the
+// reference's error taxonomy, the per-handle device workspace + ledger, and
+// the launch plans of the forward / backward passes.
+#include <algorithm>
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <string>
+
+#include "../../include/fce/fce.h"
+#include "fce_internal.h"
+
+using namespace fce;
+
+namespace {
+
+thread_local std::string g_last_error;
+
+fce_status fail(fce_status s, const char* fmt, ...) {
+    char buf[512];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, sizeof(buf), fmt, ap);
+    va_end(ap);
+    g_last_error = buf;
+    return s;
+}
+
+#define FCE_CUDA(call)                                                                          \
+    do {                                                                                        \
+        cudaError_t e_ = (call);                                                                \
+        if (e_ != cudaSuccess)                                                                  \
+            return fail(FCE_CUDA_ERROR, "%s failed: %s", #call, cudaGetErrorString(e_));        \
+    } while (0)
+
+int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
+int64_t round_up(int64_t a, int64_t b) { return ceil_div(a, b) * b; }
+
+}  // namespace
+
+struct fce_handle_s {
+    int device = 0;
+    cudaStream_t stream = nullptr;
+    int sms = 148;
+    // scratch workspace (grow-only) + the persistent small block
+    void* ws = nullptr;
+    size_t ws_size = 0;
+    size_t ws_peak = 0;
+    size_t ws_in_use = 0;
+    int* err = nullptr;                     // kErrSlots ints
+    unsigned long long* count = nullptr;    // valid-target count
+    int* host_err = nullptr;                // pinned mirror
+    int64_t splits = 0, band_cols = 0, row_chunk = 0, validate = 1;
+    int64_t launches = 0;
+};
+
+namespace fce {
+cudaStream_t handle_stream(fce_handle h) { return h ? h->stream : nullptr; }
+}  // namespace fce
+
+namespace {
+
+struct Scratch {
+    fce_handle h;
+    size_t off = 0;
+    explicit Scratch(fce_handle hh) : h(hh) {}
+    // Carves 256-byte aligned pieces out of the handle workspace; call
+    // commit() once the layout is known so the workspace grows in one go.
+    size_t take(size_t bytes) {
+        size_t o = (off + 255) & ~size_t(255);
+        off = o + bytes;
+        return o;
+    }
+    fce_status commit() {
+        if (off > h->ws_size) {
+            if (h->ws) {
+                cudaStreamSynchronize(h->stream);
+                cudaFree(h->ws);
+                h->ws = nullptr;
+                h->ws_size = 0;
+            }
+            cudaError_t e = cudaMalloc(&h->ws, off);
+            if (e != cudaSuccess)
+                return fail(FCE_CUDA_ERROR, "workspace allocation of %zu bytes failed: %s", off,
+                            cudaGetErrorString(e));
+            h->ws_size = off;
+        }
+        h->ws_in_use = off;
+        h->ws_peak = std::max(h->ws_peak, off + 64 + 3 * sizeof(int) * kErrSlots);
+        return FCE_OK;
+    }
+    template <typename T>
+    T* ptr(size_t o) const {
+        return reinterpret_cast<T*>(static_cast<char*>(h->ws) + o);
+    }
+};
+
+fce_status check_handle(fce_handle h) {
+    if (!h) return fail(FCE_INVALID_ARGUMENT, "null handle");
+    cudaError_t e = cudaSetDevice(h->device);
+    if (e != cudaSuccess) return fail(FCE_CUDA_ERROR, "cudaSetDevice: %s", cudaGetErrorString(e));
+    return FCE_OK;
+}
+
+bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
+
+// validate_problem (dense_matrix.hpp:182-211) for what the host can see, plus
+// the TMA layout contract of the device path.
+fce_status check_problem(const fce_problem* p) {
+    if (!p) return fail(FCE_INVALID_ARGUMENT, "null problem");
+    if (p->n <= 0 || p->d <= 0 || p->v <= 0)
+        return fail(FCE_EMPTY_INPUT, "problem requires N > 0, d > 0, V > 0 (got N=%lld, d=%lld, V=%lld)",
+                    (long long)p->n, (long long)p->d, (long long)p->v);
+    if (!p->hidden || !p->weight || !p->targets)
+        return fail(FCE_INVALID_ARGUMENT, "null hidden / weight / targets pointer");
+    if (p->ldh < p->d || p->ldw < p->d)
+        return fail(FCE_DIMENSION_MISMATCH, "leading dimension smaller than d (ldh=%lld ldw=%lld d=%lld)",
+                    (long long)p->ldh, (long long)p->ldw, (long long)p->d);
+    if (p->ldh % 8 || p->ldw % 8 || !aligned16(p->hidden) || !aligned16(p->weight))
+        return fail(FCE_INVALID_LAYOUT,
+                    "bf16 operands need ld %% 8 == 0 and 16-byte aligned bases (TMA); ldh=%lld ldw=%lld",
+                    (long long)p->ldh, (long long)p->ldw);
+    if (p->v_offset < 0 || (p->v_total && p->v_offset + p->v > p->v_total))
+        return fail(FCE_INVALID_LAYOUT, "vocab shard [%lld, %lld) outside [0, %lld)",
+                    (long long)p->v_offset, (long long)(p->v_offset + p->v), (long long)p->v_total);
+    if (p->n > INT32_MAX / 2 || p->v > INT32_MAX / 2 || p->d > (1 << 20))
+        return fail(FCE_INVALID_LAYOUT, "problem too large for 32-bit tile indices");
+    return FCE_OK;
+}
+
+fce_status read_errors(fce_handle h, bool sync) {
+    if (!sync) return FCE_OK;
+    FCE_CUDA(cudaMemcpyAsync(h->host_err, h->err, sizeof(int) * kErrSlots, cudaMemcpyDeviceToHost,
+                             h->stream));
+    FCE_CUDA(cudaStreamSynchronize(h->stream));
+    if (h->host_err[kErrTargetRange])
+        return fail(FCE_TARGET_OUT_OF_RANGE, "a non-ignored target lies outside [0, V)");
+    if (h->host_err[kErrDuplicate])
+        return fail(FCE_DUPLICATE_TARGET, "both stats claim the target logit");
+    if (h->host_err[kErrNotFound])
+        return fail(FCE_TARGET_OUT_OF_RANGE, "target of a position not covered by any shard");
+    if (h->host_err[kErrMissingStats])
+        return fail(FCE_MISSING_STATS, "a non-ignored position has no usable forward stats");
+    if (h->host_err[kErrOffGrid])
+        return fail(FCE_INVALID_LAYOUT, "input value is not on the bf16 grid");
+    return FCE_OK;
+}
+
+fce_status reset_flags(fce_handle h) {
+    FCE_CUDA(cudaMemsetAsync(h->err, 0, sizeof(int) * kErrSlots + 64, h->stream));
+    return FCE_OK;
+}
+
+// Forward split-V factor: units = m_blocks * splits spread over the SMs of a
+// persistent grid; pick the factor with the best tile balance.
+int choose_splits(int64_t m_blocks, int64_t v_tiles, int sms, int64_t requested) {
+    if (requested > 0) return static_cast<int>(std::min<int64_t>(requested, v_tiles));
+    int best = 1;
+    double best_eff = -1.0;
+    const int64_t max_s = std::min<int64_t>(v_tiles, 256);
+    for (int64_t s = 1; s <= max_s; ++s) {
+        const int64_t units = m_blocks * s;
+        const int64_t per_cta = ceil_div(units, sms);
+        const int64_t tiles_per_unit = ceil_div(v_tiles, s);
+        const double eff = static_cast<double>(m_blocks * v_tiles) /
+                           static_cast<double>(sms * per_cta * tiles_per_unit);
+        // prefer fewer splits when efficiency is within noise (less merge work)
+        if (eff > best_eff + 0.005) {
+            best_eff = eff;
+            best = static_cast<int>(s);
+        }
+    }
+    return best;
+}
+
+fce_status run_forward_tiles(fce_handle h, const fce_problem* p, int splits, float* pm, float* pa,
+                             float* pzt, uint8_t* pf) {
+    TileParams tp;
+    std::memset(&tp, 0, sizeof(tp));
+    TensorMaps maps;
+    std::memset(&maps, 0, sizeof(maps));
+    if (!encode_map_2d(&maps.a0, p->hidden, p->d, p->n, p->ldh * 2, kBK, kBM) ||
+        !encode_map_2d(&maps.b0, p->weight, p->d, p->v, p->ldw * 2, kBK, kBN))
+        return fail(FCE_CUDA_ERROR, "cuTensorMapEncodeTiled failed for H / W");
+    tp.mode = kEpiForward;
+    tp.n_rows = static_cast<int>(p->n);
+    tp.v_cols = static_cast<int>(p->v);
+    tp.m_blocks = static_cast<int>(ceil_div(p->n, kBM));
+    tp.v_tiles = static_cast<int>(ceil_div(p->v, kBN));
+    tp.splits = splits;
+    tp.m_group = std::min(tp.m_blocks, 16);
+    tp.k_blocks = static_cast<int>(ceil_div(p->d, kBK));
+    tp.units = tp.m_blocks * tp.splits;
+    tp.targets = p->targets;
+    tp.col_global0 = p->v_offset;
+    tp.has_ignore = p->has_ignore;
+    tp.ignore_index = p->ignore_index;
+    tp.part_m = pm;
+    tp.part_a = pa;
+    tp.part_zt = pzt;
+    tp.part_found = pf;
+    cudaError_t e = launch_tile_kernel(tp, maps, h->sms, h->stream);
+    if (e != cudaSuccess) return fail(FCE_CUDA_ERROR, "forward tile kernel: %s", cudaGetErrorString(e));
+    h->launches += 1;
+    return FCE_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* fce_last_error(void) { return g_last_error.c_str(); }
+
+const char* fce_status_string(fce_status s) {
+    switch (s) {
+        case FCE_OK: return "ok";
+        case FCE_DIMENSION_MISMATCH: return "DimensionMismatch";
+        case FCE_TARGET_OUT_OF_RANGE: return "TargetOutOfRange";
+        case FCE_UNDERFLOW_RELEASE: return "UnderflowRelease";
+        case FCE_DUPLICATE_TARGET: return "DuplicateTarget";
+        case FCE_MISSING_STATS: return "MissingStats";
+        case FCE_INCONSISTENT_UPSTREAM: return "InconsistentUpstream";
+        case FCE_UNSUPPORTED_REDUCTION: return "UnsupportedReduction";
+        case FCE_INVALID_LAYOUT: return "InvalidLayout";
+        case FCE_EMPTY_GRID: return "EmptyGrid";
+        case FCE_EMPTY_INPUT: return "EmptyInput";
+        case FCE_CUDA_ERROR: return "CudaError";
+        case FCE_NCCL_ERROR: return "NcclError";
+        case FCE_INVALID_ARGUMENT: return "InvalidArgument";
+    }
+    return "unknown";
+}
+
+fce_status fce_create(fce_handle* out, int device, void* stream) {
+    if (!out) return fail(FCE_INVALID_ARGUMENT, "null output handle");
+    *out = nullptr;
+    int count = 0;
+    cudaError_t e = cudaGetDeviceCount(&count);
+    if (e != cudaSuccess || count == 0)
+        return fail(FCE_CUDA_ERROR, "no CUDA device available (%s); the fused LCE operator has no CPU path",
+                    cudaGetErrorString(e));
+    if (device < 0 || device >= count) return fail(FCE_INVALID_ARGUMENT, "device %d out of range", device);
+    FCE_CUDA(cudaSetDevice(device));
+    cudaDeviceProp prop;
+    FCE_CUDA(cudaGetDeviceProperties(&prop, device));
+    if (prop.major != 10)
+        return fail(FCE_CUDA_ERROR, "device %d is sm_%d%d; this library is built for sm_100a only",
+                    device, prop.major, prop.minor);
+    fce_handle h = new fce_handle_s();
+    h->device = device;
+    h->stream = static_cast<cudaStream_t>(stream);
+    h->sms = prop.multiProcessorCount;
+    e = cudaMalloc(&h->err, sizeof(int) * kErrSlots + 64);
+    if (e != cudaSuccess) {
+        delete h;
+        return fail(FCE_CUDA_ERROR, "cudaMalloc: %s", cudaGetErrorString(e));
+    }
+    h->count = reinterpret_cast<unsigned long long*>(reinterpret_cast<char*>(h->err) +
+                                                     sizeof(int) * kErrSlots);
+    e = cudaMallocHost(&h->host_err, sizeof(int) * kErrSlots);
+    if (e != cudaSuccess) {
+        cudaFree(h->err);
+        delete h;
+        return fail(FCE_CUDA_ERROR, "cudaMallocHost: %s", cudaGetErrorString(e));
+    }
+    *out = h;
+    return FCE_OK;
+}
+
+fce_status fce_destroy(fce_handle h) {
+    if (!h) return FCE_OK;
+    cudaSetDevice(h->device);
+    cudaStreamSynchronize(h->stream);
+    if (h->ws) cudaFree(h->ws);
+    if (h->err) cudaFree(h->err);
+    if (h->host_err) cudaFreeHost(h->host_err);
+    delete h;
+    return FCE_OK;
+}
+
+fce_status fce_set_stream(fce_handle h, void* stream) {
+    if (!h) return fail(FCE_INVALID_ARGUMENT, "null handle");
+    h->stream = static_cast<cudaStream_t>(stream);
+    return FCE_OK;
+}
+
+fce_status fce_set_option(fce_handle h, const char* key, int64_t value) {
+    if (!h || !key) return fail(FCE_INVALID_ARGUMENT, "null handle or key");
+    if (value < 0) return fail(FCE_INVALID_ARGUMENT, "option %s must be >= 0", key);
+    if (!std::strcmp(key, "splits")) {
+        h->splits = value;
+    } else if (!std::strcmp(key, "band_cols")) {
+        if (value % kBN) return fail(FCE_INVALID_LAYOUT, "band_cols must be a multiple of %d", kBN);
+        h->band_cols = value;
+    } else if (!std::strcmp(key, "row_chunk")) {
+        if (value % kBM) return fail(FCE_INVALID_LAYOUT, "row_chunk must be a multiple of %d", kBM);
+        h->row_chunk = value;
+    } else if (!std::strcmp(key, "validate")) {
+        h->validate = value ? 1 : 0;
+    } else {
+        return fail(FCE_INVALID_ARGUMENT, "unknown option '%s'", key);
+    }
+    return FCE_OK;
+}
+
+fce_status fce_workspace_bytes(fce_handle h, size_t* current, size_t* peak) {
+    if (!h) return fail(FCE_INVALID_ARGUMENT, "null handle");
+    if (current) *current = h->ws_size + sizeof(int) * kErrSlots + 64;
+    if (peak) *peak = h->ws_peak;
+    return FCE_OK;
+}
+
+fce_status fce_launch_count(fce_handle h, int64_t* count) {
+    if (!h || !count) return fail(FCE_INVALID_ARGUMENT, "null argument");
+    *count = h->launches;
+    return FCE_OK;
+}
+
+fce_status fce_forward(fce_handle h, const fce_problem* p, int reduction, int64_t window,
+                       fce_stats stats, float* lse, float* loss_rows, float* loss_reduced) {
+    fce_status s = check_handle(h);
+    if (s) return s;
+    if ((s = check_problem(p))) return s;
+    if (reduction < 0 || reduction > 2) return fail(FCE_UNSUPPORTED_REDUCTION, "unknown reduction %d", reduction);
+    if (window < 0) return fail(FCE_INVALID_LAYOUT, "window size must be at least 1");
+    const int64_t v_total = p->v_total ? p->v_total : p->v;
+    if ((s = reset_flags(h))) return s;
+    cudaError_t e = launch_prep_targets(p->targets, p->n, p->has_ignore, p->ignore_index, v_total,
+                                        h->err, h->count, h->stream);
+    if (e != cudaSuccess) return fail(FCE_CUDA_ERROR, "prep kernel: %s", cudaGetErrorString(e));
+    h->launches += 1;
+    if ((s = read_errors(h, h->validate != 0))) return s;
+
+    const int64_t m_blocks = ceil_div(p->n, kBM), v_tiles = ceil_div(p->v, kBN);
+    int splits = choose_splits(m_blocks, v_tiles, h->sms, h->splits);
+    if (window > 0) splits = static_cast<int>(std::min<int64_t>(v_tiles, ceil_div(p->v, window)));
+
+    Scratch sc(h);
+    const size_t o_m = sc.take(sizeof(float) * splits * p->n);
+    const size_t o_a = sc.take(sizeof(float) * splits * p->n);
+    const size_t o_z = sc.take(sizeof(float) * splits * p->n);
+    const size_t o_f = sc.take(splits * p->n);
+    const size_t o_b = sc.take(sizeof(double) * (ceil_div(p->n, 256) + 1));
+    if ((s = sc.commit())) return s;
+
+    if ((s = run_forward_tiles(h, p, splits, sc.ptr<float>(o_m), sc.ptr<float>(o_a),
+                               sc.ptr<float>(o_z), sc.ptr<uint8_t>(o_f))))
+        return s;
+    int blocks = 0;
+    e = launch_merge_stats(splits, p->n, p->n, sc.ptr<float>(o_m), sc.ptr<float>(o_a),
+                           sc.ptr<float>(o_z), sc.ptr<uint8_t>(o_f), p->targets, p->has_ignore,
+                           p->ignore_index, 1, stats.m, stats.a, stats.z_target, stats.found, lse,
+                           loss_rows, sc.ptr<double>(o_b), h->err, h->stream, &blocks);
+    if (e != cudaSuccess) return fail(FCE_CUDA_ERROR, "merge kernel: %s", cudaGetErrorString(e));
+    h->launches += 1;
+    if (reduction != FCE_REDUCTION_NONE && loss_reduced) {
+        e = launch_reduce_loss(sc.ptr<double>(o_b), blocks, h->count, reduction, loss_reduced, h->stream);
+        if (e != cudaSuccess) return fail(FCE_CUDA_ERROR, "reduce kernel: %s", cudaGetErrorString(e));
+        h->launches += 1;
+    }
+    return FCE_OK;
+}
+
+fce_status fce_forward_partial(fce_handle h, const fce_problem* p, fce_stats partial) {
+    fce_status s = check_handle(h);
+    if (s) return s;
+    if ((s = check_problem(p))) return s;
+    const int64_t v_total = p->v_total ? p->v_total : p->v;
+    if ((s = reset_flags(h))) return s;
+    cudaError_t e = launch_prep_targets(p->targets, p->n, p->has_ignore, p->ignore_index, v_total,
+                                        h->err, h->count, h->stream);
+    if (e != cudaSuccess) return fail(FCE_CUDA_ERROR, "prep kernel: %s", cudaGetErrorString(e));
+    h->launches += 1;
+    if ((s = read_errors(h, h->validate != 0))) return s;
+    const int64_t m_blocks = ceil_div(p->n, kBM), v_tiles = ceil_div(p->v, kBN);
+    const int splits = choose_splits(m_blocks, v_tiles, h->sms, h->splits);
+    Scratch sc(h);
+    const size_t o_m = sc.take(sizeof(float) * splits * p->n);
+    const size_t o_a = sc.take(sizeof(float) * splits * p->n);
+    const size_t o_z = sc.take(sizeof(float) * splits * p->n);
+    const size_t o_f = sc.take(splits * p->n);
+    if ((s = sc.commit())) return s;
+    if ((s = run_forward_tiles(h, p, splits, sc.ptr<float>(o_m), sc.ptr<float>(o_a),
+                               sc.ptr<float>(o_z), sc.ptr<uint8_t>(o_f))))
+        return s;
+    e = launch_merge_stats(splits, p->n, p->n, sc.ptr<float>(o_m), sc.ptr<float>(o_a),
+                           sc.ptr<float>(o_z), sc.ptr<uint8_t>(o_f), p->targets, p->has_ignore,
+                           p->ignore_index, 0, partial.m, partial.a, partial.z_target, partial.found,
+                           nullptr, nullptr, nullptr, h->err, h->stream, nullptr);
+    if (e != cudaSuccess) return fail(FCE_CUDA_ERROR, "merge kernel: %s", cudaGetErrorString(e));
+    h->launches += 1;
+    return FCE_OK;
+}
+
+fce_status fce_merge_partials(fce_handle h, int parts, int64_t n, int64_t part_stride,
+                              const float* m, const float* a, const float* z_target,
+                              const uint8_t* found, const int64_t* targets, int32_t has_ignore,
+                              int64_t ignore_index, int reduction, fce_stats merged, float* lse,
+                              float* loss_rows, float* loss_reduced) {
+    fce_status s = check_handle(h);
+    if (s) return s;
+    if (parts <= 0) return fail(FCE_INVALID_LAYOUT, "no partials to merge");
+    if (n <= 0) return fail(FCE_EMPTY_INPUT, "merge requires N > 0");
+    if (part_stride < n) return fail(FCE_DIMENSION_MISMATCH, "part stride smaller than N");
+    if (!m || !a || !z_target || !found || !targets) return fail(FCE_INVALID_ARGUMENT, "null partial");
+    if (reduction < 0 || reduction > 2) return fail(FCE_UNSUPPORTED_REDUCTION, "unknown reduction %d", reduction);
+    if ((s = reset_flags(h))) return s;
+    // count of valid rows (targets already validated by the rank partials)
+    cudaError_t e = launch_prep_targets(targets, n, has_ignore, ignore_index, INT64_MAX, h->err,
+                                        h->count, h->stream);
+    if (e != cudaSuccess) return fail(FCE_CUDA_ERROR, "prep kernel: %s", cudaGetErrorString(e));
+    h->launches += 1;
+    Scratch sc(h);
+    const size_t o_b = sc.take(sizeof(double) * (ceil_div(n, 256) + 1));
+    if ((s = sc.commit())) return s;
+    int blocks = 0;
+    e = launch_merge_stats(parts, n, part_stride, m, a, z_target, found, targets, has_ignore,
+                           ignore_index, 1, merged.m, merged.a, merged.z_target, merged.found, lse,
+                           loss_rows, sc.ptr<double>(o_b), h->err, h->stream, &blocks);
+    if (e != cudaSuccess) return fail(FCE_CUDA_ERROR, "merge kernel: %s", cudaGetErrorString(e));
+    h->launches += 1;
+    if (reduction != FCE_REDUCTION_NONE && loss_reduced) {
+        e = launch_reduce_loss(sc.ptr<double>(o_b), blocks, h->count, reduction, loss_reduced, h->stream);
+        if (e != cudaSuccess) return fail(FCE_CUDA_ERROR, "reduce kernel: %s", cudaGetErrorString(e));
+        h->launches += 1;
+    }
+    return read_errors(h, h->validate != 0);
+}
+
+fce_status fce_backward(fce_handle h, const fce_problem* p, fce_stats stats, int reduction,
+                        float upstream_scalar, const float* upstream_rows, float* dhidden,
+                        int64_t lddh, float* dweight, int64_t lddw, int accumulate_dhidden) {
+    fce_status s = check_handle(h);
+    if (s) return s;
+    if ((s = check_problem(p))) return s;
+    if (reduction < 0 || reduction > 2) return fail(FCE_UNSUPPORTED_REDUCTION, "unknown reduction %d", reduction);
+    if (reduction == FCE_REDUCTION_NONE && !upstream_rows)
+        return fail(FCE_INCONSISTENT_UPSTREAM, "reduction none requires a per-position upstream gradient");
+    if (reduction != FCE_REDUCTION_NONE && upstream_rows)
+        return fail(FCE_INCONSISTENT_UPSTREAM, "scalar reductions require a scalar upstream gradient");
+    if (!stats.m || !stats.a || !stats.found)
+        return fail(FCE_MISSING_STATS, "stats cache (m, a, found) is required");
+    if (dhidden && lddh < p->d) return fail(FCE_DIMENSION_MISMATCH, "lddh < d");
+    if (dweight && lddw < p->d) return fail(FCE_DIMENSION_MISMATCH, "lddw < d");
+    const int64_t v_total = p->v_total ? p->v_total : p->v;
+
+    // chunking of G = N_c x V_c bf16
+    int64_t row_chunk = h->row_chunk ? h->row_chunk : 8192;
+    row_chunk = std::min(row_chunk, round_up(p->n, kBM));
+    int64_t band = h->band_cols;
+    if (!band) {
+        // ~32 MB of G per chunk so it stays L2 resident between producer and consumers
+        band = std::max<int64_t>(kBN, ((int64_t(16) << 20) / row_chunk) / kBN * kBN);
+    }
+    band = std::min(band, round_up(p->v, kBN));
+
+    Scratch sc(h);
+    const size_t o_g = sc.take(sizeof(float) * p->n);
+    const size_t o_l = sc.take(sizeof(float) * p->n);
+    const size_t o_G = sc.take(sizeof(__nv_bfloat16) * row_chunk * band);
+    if ((s = sc.commit())) return s;
+    float* gamma = sc.ptr<float>(o_g);
+    float* lse = sc.ptr<float>(o_l);
+    __nv_bfloat16* G = sc.ptr<__nv_bfloat16>(o_G);
+
+    if ((s = reset_flags(h))) return s;
+    cudaError_t e = launch_prep_targets(p->targets, p->n, p->has_ignore, p->ignore_index, v_total,
+                                        h->err, h->count, h->stream);
+    if (e != cudaSuccess) return fail(FCE_CUDA_ERROR, "prep kernel: %s", cudaGetErrorString(e));
+    e = launch_gamma(p->n, p->targets, p->has_ignore, p->ignore_index, stats.m, stats.a, stats.found,
+                     reduction, upstream_scalar, upstream_rows, h->count, gamma, lse, h->err, h->stream);
+    if (e != cudaSuccess) return fail(FCE_CUDA_ERROR, "gamma kernel: %s", cudaGetErrorString(e));
+    h->launches += 2;
+    if ((s = read_errors(h, h->validate != 0))) return s;
+    if (!dhidden && !dweight) return FCE_OK;
+
+    const int k_blocks_d = static_cast<int>(ceil_div(p->d, kBK));
+    for (int64_t r0 = 0; r0 < p->n; r0 += row_chunk) {
+        const int64_t nc = std::min(row_chunk, p->n - r0);
+        const void* h_chunk = static_cast<const __nv_bfloat16*>(p->hidden) + r0 * p->ldh;
+        for (int64_t vb = 0; vb < p->v; vb += band) {
+            const int64_t vc = std::min(band, p->v - vb);
+            const void* w_band = static_cast<const __nv_bfloat16*>(p->weight) + vb * p->ldw;
+
+            // K2a: recompute S tiles, G = gamma (softmax - onehot) -> bf16 chunk
+            TileParams tp;
+            std::memset(&tp, 0, sizeof(tp));
+            TensorMaps maps;
+            std::memset(&maps, 0, sizeof(maps));
+            if (!encode_map_2d(&maps.a0, h_chunk, p->d, nc, p->ldh * 2, kBK, kBM) ||
+                !encode_map_2d(&maps.b0, w_band, p->d, vc, p->ldw * 2, kBK, kBN))
+                return fail(FCE_CUDA_ERROR, "cuTensorMapEncodeTiled failed (grad)");
+            tp.mode = kEpiGrad;
+            tp.n_rows = static_cast<int>(nc);
+            tp.v_cols = static_cast<int>(vc);
+            tp.m_blocks = static_cast<int>(ceil_div(nc, kBM));
+            tp.v_tiles = static_cast<int>(ceil_div(vc, kBN));
+            tp.k_blocks = k_blocks_d;
+            tp.units = tp.m_blocks * tp.v_tiles;
+            tp.targets = p->targets + r0;
+            tp.col_global0 = p->v_offset + vb;
+            tp.has_ignore = p->has_ignore;
+            tp.ignore_index = p->ignore_index;
+            tp.lse = lse + r0;
+            tp.gamma = gamma + r0;
+            tp.g_out = G;
+            tp.ldg = band;
+            e = launch_tile_kernel(tp, maps, h->sms, h->stream);
+            if (e != cudaSuccess) return fail(FCE_CUDA_ERROR, "grad tile kernel: %s", cudaGetErrorString(e));
+            h->launches += 1;
+
+            // K2b + K2c in one persistent launch:
+            //   prob 0: dW[vb:vb+vc] (+)= G^T . H[r0:r0+nc]   (A, B MN-major)
+            //   prob 1: dH[r0:r0+nc] (+)= G . W[vb:vb+vc]      (A K-major, B MN-major)
+            TileParams gp;
+            std::memset(&gp, 0, sizeof(gp));
+            TensorMaps gm;
+            std::memset(&gm, 0, sizeof(gm));
+            int np = 0;
+            if (dweight) {
+                GemmProblem& q = gp.prob[np];
+                if (!encode_map_2d(np ? &gm.a1 : &gm.a0, G, band, nc, band * 2, 64, 64) ||
+                    !encode_map_2d(np ? &gm.b1 : &gm.b0, h_chunk, p->d, nc, p->ldh * 2, 64, 64))
+                    return fail(FCE_CUDA_ERROR, "cuTensorMapEncodeTiled failed (dW)");
+                q.m = static_cast<int>(vc);
+                q.n = static_cast<int>(p->d);
+                q.k_blocks = static_cast<int>(ceil_div(nc, kBK));
+                q.m_tiles = static_cast<int>(ceil_div(vc, kBM));
+                q.n_tiles = static_cast<int>(ceil_div(p->d, kBN));
+                q.a_mn = 1;
+                q.b_mn = 1;
+                q.n_fastest = 0;
+                q.accumulate = r0 > 0 ? 1 : 0;
+                q.c = dweight + vb * lddw;
+                q.ldc = lddw;
+                ++np;
+            }
+            if (dhidden) {
+                GemmProblem& q = gp.prob[np];
+                if (!encode_map_2d(np ? &gm.a1 : &gm.a0, G, band, nc, band * 2, kBK, kBM) ||
+                    !encode_map_2d(np ? &gm.b1 : &gm.b0, w_band, p->d, vc, p->ldw * 2, 64, 64))
+                    return fail(FCE_CUDA_ERROR, "cuTensorMapEncodeTiled failed (dH)");
+                q.m = static_cast<int>(nc);
+                q.n = static_cast<int>(p->d);
+                q.k_blocks = static_cast<int>(ceil_div(vc, kBK));
+                q.m_tiles = static_cast<int>(ceil_div(nc, kBM));
+                q.n_tiles = static_cast<int>(ceil_div(p->d, kBN));
+                q.a_mn = 0;
+                q.b_mn = 1;
+                q.n_fastest = 1;
+                q.accumulate = (vb > 0 || accumulate_dhidden) ? 1 : 0;
+                q.c = dhidden + r0 * lddh;
+                q.ldc = lddh;
+                ++np;
+            }
+            gp.mode = kEpiGemm;
+            gp.units0 = gp.prob[0].m_tiles * gp.prob[0].n_tiles;
+            gp.units = gp.units0 + (np > 1 ? gp.prob[1].m_tiles * gp.prob[1].n_tiles : 0);
+            e = launch_tile_kernel(gp, gm, h->sms, h->stream);
+            if (e != cudaSuccess) return fail(FCE_CUDA_ERROR, "gemm tile kernel: %s", cudaGetErrorString(e));
+            h->launches += 1;
+        }
+    }
+    return FCE_OK;
+}
+
+fce_status fce_scale(fce_handle h, float* x, int64_t count, float factor) {
+    fce_status s = check_handle(h);
+    if (s) return s;
+    if (count <= 0) return FCE_OK;
+    if (!x) return fail(FCE_INVALID_ARGUMENT, "null buffer");
+    cudaError_t e = launch_scale(x, count, nullptr, factor, h->stream);
+    if (e != cudaSuccess) return fail(FCE_CUDA_ERROR, "scale kernel: %s", cudaGetErrorString(e));
+    h->launches += 1;
+    return FCE_OK;
+}
+
+fce_status fce_generate_instance(fce_handle h, int64_t n, int64_t d, int64_t v, uint64_t seed,
+                                 void* hidden_bf16, int64_t ldh, void* weight_bf16, int64_t ldw,
+                                 int64_t* targets, int64_t ignore_index, double ignore_fraction,
+                                 float* hidden_f32, float* weight_f32) {
+    fce_status s = check_handle(h);
+    if (s) return s;
+    if (n <= 0 || d <= 0 || v <= 0) return fail(FCE_EMPTY_INPUT, "instance requires N > 0, d > 0, V > 0");
+    if (ldh < d || ldw < d) return fail(FCE_DIMENSION_MISMATCH, "leading dimension < d");
+    const double scale = 1.0 / std::sqrt(static_cast<double>(d));
+    cudaError_t e;
+    if (hidden_bf16 || hidden_f32) {
+        if (hidden_bf16) FCE_CUDA(cudaMemsetAsync(hidden_bf16, 0, sizeof(__nv_bfloat16) * n * ldh, h->stream));
+        e = launch_gen_matrix(static_cast<__nv_bfloat16*>(hidden_bf16), n, d, ldh, seed, scale,
+                              hidden_f32, h->stream);
+        if (e != cudaSuccess) return fail(FCE_CUDA_ERROR, "gen kernel: %s", cudaGetErrorString(e));
+    }
+    if (weight_bf16 || weight_f32) {
+        if (weight_bf16) FCE_CUDA(cudaMemsetAsync(weight_bf16, 0, sizeof(__nv_bfloat16) * v * ldw, h->stream));
+        e = launch_gen_matrix(static_cast<__nv_bfloat16*>(weight_bf16), v, d, ldw,
+                              seed ^ 0xA5A5A5A5A5A5A5A5ull, scale, weight_f32, h->stream);
+        if (e != cudaSuccess) return fail(FCE_CUDA_ERROR, "gen kernel: %s", cudaGetErrorString(e));
+    }
+    if (targets) {
+        e = launch_gen_targets(targets, n, v, seed, ignore_index, ignore_fraction, h->stream);
+        if (e != cudaSuccess) return fail(FCE_CUDA_ERROR, "gen kernel: %s", cudaGetErrorString(e));
+    }
+    return FCE_OK;
+}
+
+fce_status fce_f32_to_bf16(fce_handle h, const float* in, int64_t rows, int64_t cols,
+                           int64_t ld_in, void* out, int64_t ld_out) {
+    fce_status s = check_handle(h);
+    if (s) return s;
+    if (rows <= 0 || cols <= 0) return FCE_OK;
+    if (!in || !out) return fail(FCE_INVALID_ARGUMENT, "null buffer");
+    if (ld_out < cols || ld_in < cols) return fail(FCE_DIMENSION_MISMATCH, "leading dimension < cols");
+    if ((s = reset_flags(h))) return s;
+    cudaError_t e = launch_f32_to_bf16(in, rows, cols, ld_in, static_cast<__nv_bfloat16*>(out),
+                                       ld_out, h->err, h->stream);
+    if (e != cudaSuccess) return fail(FCE_CUDA_ERROR, "convert kernel: %s", cudaGetErrorString(e));
+    return read_errors(h, true);
+}
+
+}  // extern "C"

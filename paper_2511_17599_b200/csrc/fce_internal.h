@@ -1,0 +1,117 @@
+// Internal (non-ABI) declarations shared by the C-ABI layer and the CUDA
+// translation units.  Nothing here is exported from libfce.so.
+#pragma once
+
+#include <cstdint>
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <cuda_bf16.h>
+
+#include "../../include/fce/fce.h"
+
+namespace fce {
+
+// Tile geometry of the tcgen05 kernel (one CTA per SM, 1-CTA UMMA).
+constexpr int kBM = 128;      // rows per tile = TMEM lanes
+constexpr int kBN = 256;      // columns per tile = UMMA N = TMEM columns per accumulator
+constexpr int kBK = 64;       // K per pipeline stage = one 128-byte swizzle atom of bf16
+constexpr int kStages = 4;    // TMA -> MMA smem ring depth
+constexpr int kThreads = 256; // warp0 TMA, warp1 MMA, warp2 TMEM alloc, warp3 idle, warps4-7 epilogue
+constexpr int kStageBytesA = kBM * kBK * 2;
+constexpr int kStageBytesB = kBN * kBK * 2;
+constexpr int kSmemBytes = kStages * (kStageBytesA + kStageBytesB) + 1024 /*align*/ + 256 /*barriers*/;
+
+enum EpilogueMode : int { kEpiForward = 0, kEpiGrad = 1, kEpiGemm = 2 };
+
+// One GEMM problem C[M,N] (+)= A[M,K] * B[N,K]^T for the generic epilogue.
+struct GemmProblem {
+    int m, n, k_blocks;
+    int m_tiles, n_tiles;
+    int a_mn, b_mn;     // 1 = operand stored MN-major (M/N contiguous), 0 = K-major
+    int n_fastest;      // tile order inside the problem
+    int accumulate;     // 1 = red.global.add into C, 0 = plain store
+    float* c;
+    int64_t ldc;
+};
+
+struct TileParams {
+    int mode;
+    int units;               // total work units
+    // forward / grad (A = H [N, D] K-major, B = W rows K-major)
+    int n_rows;              // N
+    int v_cols;              // valid columns of this launch (V_local for fwd, band width for grad)
+    int m_blocks;            // ceil(N / kBM)
+    int v_tiles;             // ceil(v_cols / kBN)
+    int splits;              // forward split-V factor
+    int m_group;             // m-blocks per L2 raster group
+    int k_blocks;            // ceil(D / kBK)
+    const int64_t* targets;  // [N] global target ids
+    int64_t col_global0;     // global vocab id of launch column 0
+    int has_ignore;
+    int64_t ignore_index;
+    float* part_m;           // [splits][N]
+    float* part_a;
+    float* part_zt;
+    uint8_t* part_found;
+    const float* lse;        // [N] (grad)
+    const float* gamma;      // [N] (grad)
+    __nv_bfloat16* g_out;    // grad: G band [N][ldg]
+    int64_t ldg;
+    // generic GEMM (two problems in one persistent launch)
+    GemmProblem prob[2];
+    int units0;
+};
+
+struct TensorMaps {
+    CUtensorMap a0, b0, a1, b1;
+};
+
+// Stream a handle launches on (fce_api.cpp).
+cudaStream_t handle_stream(fce_handle h);
+
+// Host helpers (fce_kernels.cu)
+bool encode_map_2d(CUtensorMap* map, const void* base, uint64_t inner, uint64_t outer,
+                   uint64_t row_stride_bytes, uint32_t box_inner, uint32_t box_outer);
+cudaError_t launch_tile_kernel(const TileParams& p, const TensorMaps& maps, int grid,
+                               cudaStream_t stream);
+int device_sm_count(int device);
+
+cudaError_t launch_prep_targets(const int64_t* targets, int64_t n, int has_ignore,
+                                int64_t ignore_index, int64_t v_total, int* err_flags,
+                                unsigned long long* valid_count, cudaStream_t stream);
+cudaError_t launch_merge_stats(int parts, int64_t n, int64_t part_stride, const float* pm,
+                               const float* pa, const float* pzt, const uint8_t* pf,
+                               const int64_t* targets, int has_ignore, int64_t ignore_index,
+                               int emit_loss, float* m, float* a, float* zt, uint8_t* found,
+                               float* lse, float* loss_rows, double* block_sums, int* err_flags,
+                               cudaStream_t stream, int* blocks_out);
+cudaError_t launch_reduce_loss(const double* block_sums, int blocks,
+                               const unsigned long long* valid_count, int reduction,
+                               float* loss_reduced, cudaStream_t stream);
+cudaError_t launch_gamma(int64_t n, const int64_t* targets, int has_ignore, int64_t ignore_index,
+                         const float* m, const float* a, const uint8_t* found, int reduction,
+                         float upstream_scalar, const float* upstream_rows,
+                         const unsigned long long* valid_count, float* gamma, float* lse,
+                         int* err_flags, cudaStream_t stream);
+cudaError_t launch_scale(float* x, int64_t count, const float* factor_dev, float factor,
+                         cudaStream_t stream);
+cudaError_t launch_gen_matrix(__nv_bfloat16* out, int64_t rows, int64_t cols, int64_t ld,
+                              uint64_t seed_state, double scale, float* out_f32,
+                              cudaStream_t stream);
+cudaError_t launch_gen_targets(int64_t* out, int64_t n, int64_t v, uint64_t seed,
+                               int64_t ignore_index, double ignore_fraction, cudaStream_t stream);
+cudaError_t launch_f32_to_bf16(const float* in, int64_t rows, int64_t cols, int64_t ld_in,
+                               __nv_bfloat16* out, int64_t ld_out, int* err_flags,
+                               cudaStream_t stream);
+
+// err_flags slots
+enum ErrSlot : int {
+    kErrTargetRange = 0,
+    kErrDuplicate = 1,
+    kErrNotFound = 2,
+    kErrMissingStats = 3,
+    kErrOffGrid = 4,
+    kErrSlots = 8
+};
+
+}  // namespace fce

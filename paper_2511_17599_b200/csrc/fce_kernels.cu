@@ -1,0 +1,706 @@
+// sm_100a kernels of the fused linear-cross-entropy operator.
+//
+// One warp-specialised, persistent tcgen05 kernel template serves every
+// contraction on the path; only its epilogue differs:
+//
+//   kEpiForward  S = H_m . W_v^T tile in TMEM -> online max / sum-exp over the
+//                vocab tiles of a split + target-logit gather, written as one
+//                (m, a, z_target, found) partial per row and split.  This is
+//                Alg. 1 / accumulate_stats_block
+//                (reference proj/include/fusedce/fused_forward.hpp:47-73) with
+//                the dot products of detail::dot (detail/kernels.hpp:47-61)
+//                replaced by UMMA tiles.  No N x V buffer exists.
+//   kEpiGrad     recomputed S tile -> G = gamma * (exp(S - lse) - onehot) in
+//                registers -> bf16 G band (Alg. 2, fused_backward.hpp:34-55).
+//   kEpiGemm     plain C (+)= A . B^T with fp32 store or red.global.add; used
+//                for dW_band = G_band^T . H and dH += G_band . W_band.
+//
+// Roles (256 threads, 1 CTA / SM): warp 0 lane 0 issues TMA into a 4-stage
+// smem ring, warp 1 lane 0 issues tcgen05.mma (M=128, N=256, K=16) into one
+// of two TMEM accumulators (2 x 256 fp32 columns), warp 2 owns the TMEM
+// allocation, warps 4-7 drain TMEM with tcgen05.ld (thread = row).
+#include <cmath>
+#include <cstdio>
+#include <cudaTypedefs.h>
+
+#include "fce_internal.h"
+#include "sm100_ptx.cuh"
+
+namespace fce {
+
+using namespace ptx;
+
+static constexpr float kLog2e = 1.4426950408889634f;
+
+struct Unit {
+    int prob, m_blk, n_tile0, n_tiles, split;
+};
+
+__device__ __forceinline__ Unit get_unit(const TileParams& p, int u) {
+    Unit r;
+    r.prob = 0;
+    r.split = 0;
+    r.n_tiles = 1;
+    if (p.mode == kEpiForward) {
+        // L2 raster: groups of m_group row blocks; inside a group the split
+        // index is slow and the row block fast, so the CTAs running at the
+        // same time share one vocab range (W tiles hit in L2) and the group's
+        // H rows stay L2 resident.
+        const int per_group = p.m_group * p.splits;
+        const int g = u / per_group;
+        const int gsize = min(p.m_group, p.m_blocks - g * p.m_group);
+        const int local = u - g * per_group;
+        const int s = local / gsize;
+        const int mi = local - s * gsize;
+        r.m_blk = g * p.m_group + mi;
+        r.split = s;
+        const int t0 = static_cast<int>(static_cast<long long>(s) * p.v_tiles / p.splits);
+        const int t1 = static_cast<int>(static_cast<long long>(s + 1) * p.v_tiles / p.splits);
+        r.n_tile0 = t0;
+        r.n_tiles = t1 - t0;
+    } else if (p.mode == kEpiGrad) {
+        r.m_blk = u / p.v_tiles;
+        r.n_tile0 = u - r.m_blk * p.v_tiles;
+    } else {
+        const int pi = u < p.units0 ? 0 : 1;
+        const int local = pi ? u - p.units0 : u;
+        const GemmProblem& q = p.prob[pi];
+        if (q.n_fastest) {
+            r.m_blk = local / q.n_tiles;
+            r.n_tile0 = local - r.m_blk * q.n_tiles;
+        } else {
+            r.n_tile0 = local / q.m_tiles;
+            r.m_blk = local - r.n_tile0 * q.m_tiles;
+        }
+        r.prob = pi;
+    }
+    return r;
+}
+
+template <int EPI>
+__global__ void __launch_bounds__(kThreads, 1)
+    fce_tile_kernel(const __grid_constant__ TileParams p, const __grid_constant__ TensorMaps maps) {
+    extern __shared__ uint8_t smem_raw[];
+    const uint32_t raw_addr = smem_u32(smem_raw);
+    uint8_t* smem = smem_raw + (((raw_addr + 1023u) & ~1023u) - raw_addr);
+    uint8_t* sA = smem;
+    uint8_t* sB = smem + kStages * kStageBytesA;
+    uint64_t* bars = reinterpret_cast<uint64_t*>(sB + kStages * kStageBytesB);
+    uint64_t* full = bars;
+    uint64_t* empty = bars + kStages;
+    uint64_t* tfull = bars + 2 * kStages;
+    uint64_t* tempty = tfull + 2;
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+
+    const int warp = threadIdx.x >> 5;
+    const int lane = threadIdx.x & 31;
+
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < kStages; ++s) {
+            mbar_init(&full[s], 1);
+            mbar_init(&empty[s], 1);
+        }
+        for (int b = 0; b < 2; ++b) {
+            mbar_init(&tfull[b], 1);
+            mbar_init(&tempty[b], 4);
+        }
+        fence_mbar_init();
+    }
+    if (warp == 0 && lane == 0) {
+        tma_prefetch_desc(&maps.a0);
+        tma_prefetch_desc(&maps.b0);
+        if (EPI == kEpiGemm) {
+            tma_prefetch_desc(&maps.a1);
+            tma_prefetch_desc(&maps.b1);
+        }
+    }
+    if (warp == 2) {
+        tmem_alloc<512>(tmem_slot);
+    }
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem_base = *tmem_slot;
+
+    if (warp == 0) {
+        // ------------------------------------------------------------ TMA producer
+        if (lane == 0) {
+            int stage = 0;
+            uint32_t phase = 0;
+            for (int u = blockIdx.x; u < p.units; u += gridDim.x) {
+                const Unit un = get_unit(p, u);
+                const CUtensorMap* ma = un.prob ? &maps.a1 : &maps.a0;
+                const CUtensorMap* mb = un.prob ? &maps.b1 : &maps.b0;
+                int kbs = p.k_blocks, a_mn = 0, b_mn = 0;
+                if (EPI == kEpiGemm) {
+                    kbs = p.prob[un.prob].k_blocks;
+                    a_mn = p.prob[un.prob].a_mn;
+                    b_mn = p.prob[un.prob].b_mn;
+                }
+                for (int t = 0; t < un.n_tiles; ++t) {
+                    const int n_tile = un.n_tile0 + t;
+                    for (int kb = 0; kb < kbs; ++kb) {
+                        mbar_wait(&empty[stage], phase ^ 1);
+                        mbar_arrive_expect_tx(&full[stage], kStageBytesA + kStageBytesB);
+                        uint8_t* a_dst = sA + stage * kStageBytesA;
+                        uint8_t* b_dst = sB + stage * kStageBytesB;
+                        if (!a_mn) {
+                            tma_load_2d(a_dst, ma, &full[stage], kb * kBK, un.m_blk * kBM,
+                                        kEvictNormal);
+                        } else {
+#pragma unroll
+                            for (int j = 0; j < kBM / 64; ++j)
+                                tma_load_2d(a_dst + j * 8192, ma, &full[stage],
+                                            un.m_blk * kBM + 64 * j, kb * kBK, kEvictNormal);
+                        }
+                        if (!b_mn) {
+                            tma_load_2d(b_dst, mb, &full[stage], kb * kBK, n_tile * kBN,
+                                        kEvictNormal);
+                        } else {
+#pragma unroll
+                            for (int j = 0; j < kBN / 64; ++j)
+                                tma_load_2d(b_dst + j * 8192, mb, &full[stage],
+                                            n_tile * kBN + 64 * j, kb * kBK, kEvictNormal);
+                        }
+                        if (++stage == kStages) {
+                            stage = 0;
+                            phase ^= 1;
+                        }
+                    }
+                }
+            }
+        }
+    } else if (warp == 1) {
+        // ------------------------------------------------------------ MMA issuer
+        if (lane == 0) {
+            int stage = 0;
+            uint32_t phase = 0;
+            int acc = 0;
+            uint32_t acc_phase = 0;
+            for (int u = blockIdx.x; u < p.units; u += gridDim.x) {
+                const Unit un = get_unit(p, u);
+                int kbs = p.k_blocks, a_mn = 0, b_mn = 0;
+                if (EPI == kEpiGemm) {
+                    kbs = p.prob[un.prob].k_blocks;
+                    a_mn = p.prob[un.prob].a_mn;
+                    b_mn = p.prob[un.prob].b_mn;
+                }
+                const uint32_t idesc = make_idesc_bf16(kBM, kBN, a_mn, b_mn);
+                for (int t = 0; t < un.n_tiles; ++t) {
+                    mbar_wait(&tempty[acc], acc_phase ^ 1);
+                    tc_fence_after();
+                    const uint32_t d_tmem = tmem_base + acc * kBN;
+                    for (int kb = 0; kb < kbs; ++kb) {
+                        mbar_wait(&full[stage], phase);
+                        tc_fence_after();
+                        const uint32_t a_base = smem_u32(sA + stage * kStageBytesA);
+                        const uint32_t b_base = smem_u32(sB + stage * kStageBytesB);
+#pragma unroll
+                        for (int k = 0; k < kBK / 16; ++k) {
+                            // K-major SW128: +32 B per K=16 step inside the 128-B atom.
+                            // MN-major SW128: +16 rows * 128 B = 2 KB per K=16 step;
+                            //   LBO = 8 KB between 64-wide M/N column blocks.
+                            const uint64_t ad = a_mn ? make_sdesc_sw128(a_base + k * 2048, 8192, 1024)
+                                                     : make_sdesc_sw128(a_base + k * 32, 16, 1024);
+                            const uint64_t bd = b_mn ? make_sdesc_sw128(b_base + k * 2048, 8192, 1024)
+                                                     : make_sdesc_sw128(b_base + k * 32, 16, 1024);
+                            umma_bf16(d_tmem, ad, bd, idesc, (kb | k) != 0 ? 1u : 0u);
+                        }
+                        umma_commit(&empty[stage]);
+                        if (++stage == kStages) {
+                            stage = 0;
+                            phase ^= 1;
+                        }
+                    }
+                    umma_commit(&tfull[acc]);
+                    acc ^= 1;
+                    if (acc == 0) acc_phase ^= 1;
+                }
+            }
+        }
+    } else if (warp >= 4) {
+        // ------------------------------------------------------------ epilogue
+        const int q = warp & 3;
+        const int r = q * 32 + lane;
+        int acc = 0;
+        uint32_t acc_phase = 0;
+        for (int u = blockIdx.x; u < p.units; u += gridDim.x) {
+            const Unit un = get_unit(p, u);
+            const int64_t row = static_cast<int64_t>(un.m_blk) * kBM + r;
+
+            // per-row state (forward / grad)
+            bool row_ok = false, skip = true;
+            int64_t tcol = -1;  // launch-local column of this row's target
+            float m_run = -INFINITY, a_run = 0.f, zt = 0.f;
+            bool found = false;
+            float l2lse = 0.f, gam = 0.f;
+            if (EPI != kEpiGemm) {
+                row_ok = row < p.n_rows;
+                if (row_ok) {
+                    const int64_t y = p.targets[row];
+                    skip = p.has_ignore && y == p.ignore_index;
+                    tcol = y - p.col_global0;
+                    if (EPI == kEpiGrad) {
+                        gam = skip ? 0.f : p.gamma[row];
+                        l2lse = skip ? 0.f : p.lse[row] * kLog2e;
+                    }
+                }
+            }
+
+            for (int t = 0; t < un.n_tiles; ++t) {
+                const int n_tile = un.n_tile0 + t;
+                mbar_wait(&tfull[acc], acc_phase);
+                tc_fence_after();
+                const uint32_t taddr = tmem_base + (static_cast<uint32_t>(q * 32) << 16) +
+                                       static_cast<uint32_t>(acc * kBN);
+#pragma unroll 1
+                for (int c = 0; c < kBN / 32; ++c) {
+                    float v[32];
+                    tmem_ld32(taddr + c * 32, v);
+                    const int col0 = n_tile * kBN + c * 32;
+                    if (EPI == kEpiForward) {
+                        if (col0 + 32 > p.v_cols) {
+#pragma unroll
+                            for (int j = 0; j < 32; ++j)
+                                if (col0 + j >= p.v_cols) v[j] = -INFINITY;
+                        }
+                        float cmax = v[0];
+#pragma unroll
+                        for (int j = 1; j < 32; ++j) cmax = fmaxf(cmax, v[j]);
+                        if (cmax > m_run) {
+                            a_run *= ex2((m_run - cmax) * kLog2e);
+                            m_run = cmax;
+                        }
+                        if (cmax != -INFINITY) {
+                            const float mb = m_run * kLog2e;
+                            float s0 = 0.f, s1 = 0.f;
+#pragma unroll
+                            for (int j = 0; j < 32; j += 2) {
+                                s0 += ex2(fmaf(v[j], kLog2e, -mb));
+                                s1 += ex2(fmaf(v[j + 1], kLog2e, -mb));
+                            }
+                            a_run += s0 + s1;
+                        }
+                        const int64_t tc = tcol - col0;
+                        if (tc >= 0 && tc < 32) {
+#pragma unroll
+                            for (int j = 0; j < 32; ++j)
+                                if (j == tc) zt = v[j];
+                            found = true;
+                        }
+                    } else if (EPI == kEpiGrad) {
+                        if (row_ok) {
+                            const int64_t tc = tcol - col0;
+                            uint32_t packed[16];
+#pragma unroll
+                            for (int j = 0; j < 32; j += 2) {
+                                float g0 = gam * (ex2(fmaf(v[j], kLog2e, -l2lse)) -
+                                                  (tc == j ? 1.f : 0.f));
+                                float g1 = gam * (ex2(fmaf(v[j + 1], kLog2e, -l2lse)) -
+                                                  (tc == j + 1 ? 1.f : 0.f));
+                                if (gam == 0.f || col0 + j >= p.v_cols) g0 = 0.f;
+                                if (gam == 0.f || col0 + j + 1 >= p.v_cols) g1 = 0.f;
+                                packed[j >> 1] = pack_bf16(g0, g1);
+                            }
+                            __nv_bfloat16* dst = p.g_out + row * p.ldg + col0;
+#pragma unroll
+                            for (int j = 0; j < 4; ++j)
+                                st_v4_b32(dst + 8 * j, packed[4 * j], packed[4 * j + 1],
+                                          packed[4 * j + 2], packed[4 * j + 3]);
+                        }
+                    } else {
+                        const GemmProblem& gq = p.prob[un.prob];
+                        if (row < gq.m) {
+                            float* dst = gq.c + row * gq.ldc + col0;
+                            const bool vec = (col0 + 32 <= gq.n) &&
+                                             ((reinterpret_cast<uintptr_t>(dst) & 15) == 0);
+                            if (vec) {
+                                if (gq.accumulate) {
+#pragma unroll
+                                    for (int j = 0; j < 32; j += 4)
+                                        red_add_v4(dst + j, v[j], v[j + 1], v[j + 2], v[j + 3]);
+                                } else {
+#pragma unroll
+                                    for (int j = 0; j < 32; j += 4)
+                                        st_v4(dst + j, v[j], v[j + 1], v[j + 2], v[j + 3]);
+                                }
+                            } else {
+#pragma unroll
+                                for (int j = 0; j < 32; ++j) {
+                                    if (col0 + j < gq.n) {
+                                        if (gq.accumulate)
+                                            atomicAdd(dst + j, v[j]);
+                                        else
+                                            dst[j] = v[j];
+                                    }
+                                }
+                            }
+                        }
+                    }
+                }
+                tc_fence_before();
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&tempty[acc]);
+                acc ^= 1;
+                if (acc == 0) acc_phase ^= 1;
+            }
+
+            if (EPI == kEpiForward && row_ok) {
+                const size_t off = static_cast<size_t>(un.split) * p.n_rows + row;
+                p.part_m[off] = skip ? -INFINITY : m_run;
+                p.part_a[off] = skip ? 0.f : a_run;
+                p.part_zt[off] = (skip || !found) ? 0.f : zt;
+                p.part_found[off] = (skip || !found) ? 0 : 1;
+            }
+        }
+    }
+
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    if (warp == 2) {
+        tmem_dealloc<512>(tmem_base);
+    }
+}
+
+// ============================================================== host helpers
+
+static PFN_cuTensorMapEncodeTiled_v12000 get_encode_fn() {
+    static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+    if (!fn) {
+        cudaDriverEntryPointQueryResult q;
+        void* ptr = nullptr;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &ptr, cudaEnableDefault, &q) ==
+                cudaSuccess &&
+            q == cudaDriverEntryPointSuccess) {
+            fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(ptr);
+        }
+    }
+    return fn;
+}
+
+bool encode_map_2d(CUtensorMap* map, const void* base, uint64_t inner, uint64_t outer,
+                   uint64_t row_stride_bytes, uint32_t box_inner, uint32_t box_outer) {
+    auto fn = get_encode_fn();
+    if (!fn) return false;
+    cuuint64_t dims[2] = {inner, outer};
+    cuuint64_t strides[1] = {row_stride_bytes};
+    cuuint32_t box[2] = {box_inner, box_outer};
+    cuuint32_t estr[2] = {1, 1};
+    CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims,
+                    strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                    CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    return r == CUDA_SUCCESS;
+}
+
+int device_sm_count(int device) {
+    int v = 0;
+    cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, device);
+    return v;
+}
+
+template <int EPI>
+static cudaError_t launch_one(const TileParams& p, const TensorMaps& maps, int grid,
+                              cudaStream_t stream) {
+    static bool attr_done = false;
+    if (!attr_done) {
+        cudaError_t e = cudaFuncSetAttribute(fce_tile_kernel<EPI>,
+                                             cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes);
+        if (e != cudaSuccess) return e;
+        attr_done = true;
+    }
+    fce_tile_kernel<EPI><<<grid, kThreads, kSmemBytes, stream>>>(p, maps);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_tile_kernel(const TileParams& p, const TensorMaps& maps, int grid,
+                               cudaStream_t stream) {
+    if (p.units <= 0) return cudaSuccess;
+    if (grid > p.units) grid = p.units;
+    switch (p.mode) {
+        case kEpiForward: return launch_one<kEpiForward>(p, maps, grid, stream);
+        case kEpiGrad: return launch_one<kEpiGrad>(p, maps, grid, stream);
+        default: return launch_one<kEpiGemm>(p, maps, grid, stream);
+    }
+}
+
+// ============================================================== small kernels
+
+__global__ void k_prep_targets(const int64_t* __restrict__ targets, int64_t n, int has_ignore,
+                               int64_t ignore_index, int64_t v_total, int* err,
+                               unsigned long long* valid_count) {
+    unsigned long long local = 0;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t y = targets[i];
+        if (has_ignore && y == ignore_index) continue;
+        ++local;
+        if (y < 0 || y >= v_total) atomicOr(&err[kErrTargetRange], 1);
+    }
+    // warp aggregate then one atomic per warp (integer: order-independent)
+    for (int o = 16; o > 0; o >>= 1) local += __shfl_down_sync(0xffffffffu, local, o);
+    if ((threadIdx.x & 31) == 0 && local) atomicAdd(valid_count, local);
+}
+
+cudaError_t launch_prep_targets(const int64_t* targets, int64_t n, int has_ignore,
+                                int64_t ignore_index, int64_t v_total, int* err_flags,
+                                unsigned long long* valid_count, cudaStream_t stream) {
+    int blocks = static_cast<int>(std::min<int64_t>((n + 255) / 256, 1184));
+    if (blocks < 1) blocks = 1;
+    k_prep_targets<<<blocks, 256, 0, stream>>>(targets, n, has_ignore, ignore_index, v_total,
+                                               err_flags, valid_count);
+    return cudaGetLastError();
+}
+
+// Ordered merge of `parts` partial stats per row, exactly the reference's
+// merge_stats (softmax_stats.hpp:52-75) applied in ascending part order
+// (fused_forward.hpp:112-123 for windows, parallel_sim.hpp:214-220 for
+// ranks), then loss = (m - z_t) + log a (softmax_stats.hpp:45).
+__global__ void k_merge_stats(int parts, int64_t n, int64_t stride, const float* __restrict__ pm,
+                              const float* __restrict__ pa, const float* __restrict__ pzt,
+                              const uint8_t* __restrict__ pf, const int64_t* __restrict__ targets,
+                              int has_ignore, int64_t ignore_index, int emit_loss, float* m_out,
+                              float* a_out, float* zt_out, uint8_t* f_out, float* lse_out,
+                              float* loss_rows, double* block_sums, int* err) {
+    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    double my_loss = 0.0;
+    if (i < n) {
+        const bool ign = has_ignore && targets[i] == ignore_index;
+        float M = -INFINITY, A = 0.f, Z = 0.f;
+        bool F = false;
+        if (!ign) {
+            for (int s = 0; s < parts; ++s) {
+                const int64_t o = s * stride + i;
+                const float sm = pm[o], sa = pa[o];
+                const bool sf = pf[o] != 0;
+                if (F && sf) atomicOr(&err[kErrDuplicate], 1);
+                const float nm = M > sm ? M : sm;
+                float acc = 0.f;
+                if (A != 0.f) acc += A * expf(M - nm);
+                if (sa != 0.f) acc += sa * expf(sm - nm);
+                M = nm;
+                A = acc;
+                if (!F && sf) {
+                    Z = pzt[o];
+                    F = true;
+                }
+            }
+        }
+        if (m_out) m_out[i] = M;
+        if (a_out) a_out[i] = A;
+        if (zt_out) zt_out[i] = Z;
+        if (f_out) f_out[i] = F ? 1 : 0;
+        if (emit_loss) {
+            float loss = 0.f;
+            if (!ign) {
+                if (!F) atomicOr(&err[kErrNotFound], 1);
+                loss = (M - Z) + logf(A);
+            }
+            if (loss_rows) loss_rows[i] = loss;
+            if (lse_out) lse_out[i] = M + logf(A);
+            my_loss = loss;
+        }
+    }
+    if (emit_loss && block_sums) {
+        __shared__ double red[256];
+        red[threadIdx.x] = my_loss;
+        __syncthreads();
+        for (int o = 128; o > 0; o >>= 1) {
+            if (threadIdx.x < o) red[threadIdx.x] += red[threadIdx.x + o];
+            __syncthreads();
+        }
+        if (threadIdx.x == 0) block_sums[blockIdx.x] = red[0];
+    }
+}
+
+cudaError_t launch_merge_stats(int parts, int64_t n, int64_t part_stride, const float* pm,
+                               const float* pa, const float* pzt, const uint8_t* pf,
+                               const int64_t* targets, int has_ignore, int64_t ignore_index,
+                               int emit_loss, float* m, float* a, float* zt, uint8_t* found,
+                               float* lse, float* loss_rows, double* block_sums, int* err_flags,
+                               cudaStream_t stream, int* blocks_out) {
+    const int blocks = static_cast<int>((n + 255) / 256);
+    if (blocks_out) *blocks_out = blocks;
+    k_merge_stats<<<blocks, 256, 0, stream>>>(parts, n, part_stride, pm, pa, pzt, pf, targets,
+                                              has_ignore, ignore_index, emit_loss, m, a, zt, found,
+                                              lse, loss_rows, block_sums, err_flags);
+    return cudaGetLastError();
+}
+
+// Deterministic final reduction (fixed order), then reduce_losses semantics
+// (reduction.hpp:37-54): mean over the valid count, 0 when nothing is valid.
+__global__ void k_reduce_loss(const double* __restrict__ block_sums, int blocks,
+                              const unsigned long long* valid_count, int reduction, float* out) {
+    __shared__ double red[256];
+    double s = 0.0;
+    for (int i = threadIdx.x; i < blocks; i += 256) s += block_sums[i];
+    red[threadIdx.x] = s;
+    __syncthreads();
+    for (int o = 128; o > 0; o >>= 1) {
+        if (threadIdx.x < o) red[threadIdx.x] += red[threadIdx.x + o];
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) {
+        double total = red[0];
+        if (reduction == 0) {
+            const unsigned long long c = *valid_count;
+            total = c > 0 ? total / static_cast<double>(c) : 0.0;
+        }
+        *out = static_cast<float>(total);
+    }
+}
+
+cudaError_t launch_reduce_loss(const double* block_sums, int blocks,
+                               const unsigned long long* valid_count, int reduction,
+                               float* loss_reduced, cudaStream_t stream) {
+    k_reduce_loss<<<1, 256, 0, stream>>>(block_sums, blocks, valid_count, reduction, loss_reduced);
+    return cudaGetLastError();
+}
+
+// gamma_n = effective upstream (reduction.hpp:110-126); lse_n = m + log a;
+// require_stats (fused_backward.hpp:58-73): non-ignored rows need found && a > 0.
+__global__ void k_gamma(int64_t n, const int64_t* __restrict__ targets, int has_ignore,
+                        int64_t ignore_index, const float* __restrict__ m,
+                        const float* __restrict__ a, const uint8_t* __restrict__ found,
+                        int reduction, float upstream_scalar, const float* __restrict__ up_rows,
+                        const unsigned long long* valid_count, float* gamma, float* lse,
+                        int* err) {
+    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const bool ign = has_ignore && targets[i] == ignore_index;
+    if (ign) {
+        gamma[i] = 0.f;
+        lse[i] = 0.f;
+        return;
+    }
+    if (!(found[i] != 0) || !(a[i] > 0.f)) atomicOr(&err[kErrMissingStats], 1);
+    float g;
+    if (reduction == 2) {
+        g = up_rows[i];
+    } else if (reduction == 0) {
+        const unsigned long long c = *valid_count;
+        g = c > 0 ? upstream_scalar / static_cast<float>(c) : 0.f;
+    } else {
+        g = upstream_scalar;
+    }
+    gamma[i] = g;
+    lse[i] = m[i] + logf(a[i]);
+}
+
+cudaError_t launch_gamma(int64_t n, const int64_t* targets, int has_ignore, int64_t ignore_index,
+                         const float* m, const float* a, const uint8_t* found, int reduction,
+                         float upstream_scalar, const float* upstream_rows,
+                         const unsigned long long* valid_count, float* gamma, float* lse,
+                         int* err_flags, cudaStream_t stream) {
+    const int blocks = static_cast<int>((n + 255) / 256);
+    k_gamma<<<blocks, 256, 0, stream>>>(n, targets, has_ignore, ignore_index, m, a, found,
+                                        reduction, upstream_scalar, upstream_rows, valid_count,
+                                        gamma, lse, err_flags);
+    return cudaGetLastError();
+}
+
+__global__ void k_scale(float* x, int64_t count, const float* factor_dev, float factor) {
+    const float f = factor_dev ? *factor_dev : factor;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < count;
+         i += (int64_t)gridDim.x * blockDim.x)
+        x[i] *= f;
+}
+
+cudaError_t launch_scale(float* x, int64_t count, const float* factor_dev, float factor,
+                         cudaStream_t stream) {
+    int blocks = static_cast<int>(std::min<int64_t>((count + 255) / 256, 148 * 16));
+    if (blocks < 1) blocks = 1;
+    k_scale<<<blocks, 256, 0, stream>>>(x, count, factor_dev, factor);
+    return cudaGetLastError();
+}
+
+// ------------------------------------------------- synthetic instance (device)
+// Bit-identical to make_random_instance (reference instance.hpp:38-66):
+// splitmix64 is counter based, so element i of a stream whose state starts at
+// s0 is mix(s0 + (i + 1) * golden).
+__device__ __forceinline__ uint64_t splitmix_at(uint64_t s0, uint64_t i) {
+    uint64_t z = s0 + (i + 1) * 0x9E3779B97F4A7C15ull;
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+    return z ^ (z >> 31);
+}
+
+__device__ __forceinline__ float round_bf16_dev(float x) {
+    if (isnan(x)) return x;
+    uint32_t bits = __float_as_uint(x);
+    const uint32_t lsb = (bits >> 16) & 1u;
+    bits += 0x7FFFu + lsb;
+    bits &= 0xFFFF0000u;
+    return __uint_as_float(bits);
+}
+
+__global__ void k_gen_matrix(__nv_bfloat16* out, int64_t rows, int64_t cols, int64_t ld,
+                             uint64_t s0, double scale, float* out_f32) {
+    const int64_t total = rows * cols;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        const uint64_t z = splitmix_at(s0, static_cast<uint64_t>(i));
+        const double u = static_cast<double>(z >> 11) * 0x1.0p-53;
+        const double x = __dmul_rn(__dsub_rn(__dmul_rn(2.0, u), 1.0), scale);
+        const float xf = round_bf16_dev(__double2float_rn(x));
+        const int64_t r = i / cols, c = i - r * cols;
+        if (out) out[r * ld + c] = __float2bfloat16_rn(xf);
+        if (out_f32) out_f32[r * ld + c] = xf;
+    }
+}
+
+cudaError_t launch_gen_matrix(__nv_bfloat16* out, int64_t rows, int64_t cols, int64_t ld,
+                              uint64_t seed_state, double scale, float* out_f32,
+                              cudaStream_t stream) {
+    k_gen_matrix<<<148 * 8, 256, 0, stream>>>(out, rows, cols, ld, seed_state, scale, out_f32);
+    return cudaGetLastError();
+}
+
+__global__ void k_gen_targets(int64_t* out, int64_t n, int64_t v, uint64_t seed,
+                              int64_t ignore_index, double ignore_fraction) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        int64_t t = static_cast<int64_t>(splitmix_at(seed ^ 0x5A5A5A5A5A5A5A5Aull, i) %
+                                         static_cast<uint64_t>(v));
+        if (ignore_fraction > 0.0) {
+            const double u =
+                static_cast<double>(splitmix_at(seed ^ 0x3C3C3C3C3C3C3C3Cull, i) >> 11) *
+                0x1.0p-53;
+            if (u < ignore_fraction) t = ignore_index;
+        }
+        out[i] = t;
+    }
+}
+
+cudaError_t launch_gen_targets(int64_t* out, int64_t n, int64_t v, uint64_t seed,
+                               int64_t ignore_index, double ignore_fraction, cudaStream_t stream) {
+    int blocks = static_cast<int>(std::min<int64_t>((n + 255) / 256, 1184));
+    if (blocks < 1) blocks = 1;
+    k_gen_targets<<<blocks, 256, 0, stream>>>(out, n, v, seed, ignore_index, ignore_fraction);
+    return cudaGetLastError();
+}
+
+// float (on the bf16 grid) -> bf16, flagging off-grid values (bf16.hpp:31-36).
+__global__ void k_f32_to_bf16(const float* __restrict__ in, int64_t rows, int64_t cols,
+                              int64_t ld_in, __nv_bfloat16* out, int64_t ld_out, int* err) {
+    const int64_t total = rows * ld_out;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t r = i / ld_out, c = i - r * ld_out;
+        float x = 0.f;
+        if (c < cols) {
+            x = in[r * ld_in + c];
+            if (round_bf16_dev(x) != x && !isnan(x)) atomicOr(&err[kErrOffGrid], 1);
+        }
+        out[i] = __float2bfloat16_rn(x);
+    }
+}
+
+cudaError_t launch_f32_to_bf16(const float* in, int64_t rows, int64_t cols, int64_t ld_in,
+                               __nv_bfloat16* out, int64_t ld_out, int* err_flags,
+                               cudaStream_t stream) {
+    k_f32_to_bf16<<<148 * 8, 256, 0, stream>>>(in, rows, cols, ld_in, out, ld_out, err_flags);
+    return cudaGetLastError();
+}
+
+}  // namespace fce
