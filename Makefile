@@ -2,8 +2,8 @@
 # reference-built checker.  `python -c "import __graft_entry__ as g; g.build()"`
 # runs the same targets.
 NVCC      ?= nvcc
-CXX       ?= g++
-CC        ?= gcc
+CXX       := /usr/bin/g++
+CC        := /usr/bin/gcc
 ARCH      := -gencode arch=compute_100a,code=sm_100a
 NVFLAGS   := $(ARCH) -O3 -lineinfo -std=c++17 -Xcompiler -fPIC -Xcompiler -Wall \
              --expt-relaxed-constexpr -diag-suppress 177
@@ -33,7 +33,7 @@ ref:
 
 $(REF_LIB): oracle/ref_shim.cpp
 	mkdir -p oracle/_ref
-	$(CXX) -std=c++20 -O3 -march=x86-64-v3 -fPIC -shared -pthread -Dfusedce=fusedce_ref \
+	$(CXX) -std=c++20 -O3 -march=x86-64-v3 -fPIC -shared -pthread -Dfusedce=fusedce_ref -ffp-contract=off \
 	    -I$(REF_DIR)/include -o $@ oracle/ref_shim.cpp
 
 clean:

@@ -92,13 +92,21 @@ const char* fce_last_error(void);
 const char* fce_status_string(fce_status s);
 /* Tuning / behaviour knobs: "splits" (forward split-V factor, 0 = auto),
  * "band_cols" / "row_chunk" (backward G chunk, 0 = auto), "validate"
- * (1 = sync and check targets / stats, default 1). */
+ * (1 = sync and check targets / stats, default 1), "timing" (1 = per-kernel
+ * event timing, see fce_kernel_stats; setting it resets the counters). */
 fce_status fce_set_option(fce_handle h, const char* key, int64_t value);
 /* Library-owned device workspace (the device analogue of MemoryLedger,
  * memory_ledger.hpp:18-62): bytes held now and the high-water mark. */
 fce_status fce_workspace_bytes(fce_handle h, size_t* current, size_t* peak);
 /* Number of kernels this handle launched since creation (for the bench). */
 fce_status fce_launch_count(fce_handle h, int64_t* count);
+/* With option "timing" = 1 every tile-kernel launch is bracketed by CUDA
+ * events on the handle's stream.  kernel: 0 = forward (online-LSE epilogue),
+ * 1 = gradient producer (recompute + softmax - onehot), 2 = dW / dH
+ * contractions.  Returns summed device time, launch count and algorithmic
+ * flops (2 * M * N * K per contraction) since timing was (re)enabled. */
+fce_status fce_kernel_stats(fce_handle h, int kernel, double* total_ms, int64_t* launches,
+                            double* flops);
 
 /* ---------------------------------------------------------------- forward
  * fused_forward (fused_forward.hpp:161-172); window > 0 gives

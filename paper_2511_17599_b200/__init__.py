@@ -78,7 +78,7 @@ class FceStats(ctypes.Structure):
 # Every symbol include/fce/fce.h and include/fce/fce_vp.h declare.
 EXPORTED_SYMBOLS = [
     "fce_create", "fce_destroy", "fce_set_stream", "fce_last_error", "fce_status_string",
-    "fce_set_option", "fce_workspace_bytes", "fce_launch_count", "fce_forward",
+    "fce_set_option", "fce_workspace_bytes", "fce_launch_count", "fce_kernel_stats", "fce_forward",
     "fce_forward_partial", "fce_merge_partials", "fce_backward", "fce_scale",
     "fce_generate_instance", "fce_f32_to_bf16",
     "fce_comm_unique_id", "fce_comm_init", "fce_comm_destroy", "fce_vp_last_error",
@@ -108,6 +108,7 @@ def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
         "fce_set_option": (I32, [P, ctypes.c_char_p, I64]),
         "fce_workspace_bytes": (I32, [P, ctypes.POINTER(ctypes.c_size_t), ctypes.POINTER(ctypes.c_size_t)]),
         "fce_launch_count": (I32, [P, ctypes.POINTER(I64)]),
+        "fce_kernel_stats": (I32, [P, I32, ctypes.POINTER(D), ctypes.POINTER(I64), ctypes.POINTER(D)]),
         "fce_forward": (I32, [P, ctypes.POINTER(FceProblem), I32, I64, FceStats, P, P, P]),
         "fce_forward_partial": (I32, [P, ctypes.POINTER(FceProblem), FceStats]),
         "fce_merge_partials": (I32, [P, I32, I64, I64, P, P, P, P, P, I32, I64, I32, FceStats, P, P, P]),
@@ -172,6 +173,14 @@ class Handle:
         c = ctypes.c_int64()
         _check(self.lib.fce_launch_count(self._h, ctypes.byref(c)))
         return c.value
+
+    KERNELS = {0: "fce_fwd_sm100", 1: "fce_bwd_grad_sm100", 2: "fce_bwd_gemm_sm100"}
+
+    def kernel_stats(self, kernel: int):
+        """(total device ms, launches, algorithmic flops) since timing was enabled."""
+        ms, n, fl = ctypes.c_double(), ctypes.c_int64(), ctypes.c_double()
+        _check(self.lib.fce_kernel_stats(self._h, kernel, ctypes.byref(ms), ctypes.byref(n), ctypes.byref(fl)))
+        return ms.value, n.value, fl.value
 
     def close(self):
         if self._h:

@@ -7,6 +7,7 @@
 #include <cstdio>
 #include <cstring>
 #include <string>
+#include <vector>
 
 #include "../../include/fce/fce.h"
 #include "fce_internal.h"
@@ -53,10 +54,23 @@ struct fce_handle_s {
     int* host_err = nullptr;                // pinned mirror
     int64_t splits = 0, band_cols = 0, row_chunk = 0, validate = 1;
     int64_t launches = 0;
+    // optional per-kernel CUDA-event timing of the tile kernels (bench roofline)
+    int64_t timing = 0;
+    struct Pending {
+        int mode;
+        cudaEvent_t start, stop;
+        double flops;
+    };
+    std::vector<Pending> pending;
+    std::vector<cudaEvent_t> event_pool;
+    double k_ms[3] = {0, 0, 0};
+    double k_flops[3] = {0, 0, 0};
+    int64_t k_launches[3] = {0, 0, 0};
 };
 
 namespace fce {
 cudaStream_t handle_stream(fce_handle h) { return h ? h->stream : nullptr; }
+void set_last_error(const char* msg) { g_last_error = msg; }
 }  // namespace fce
 
 namespace {
@@ -174,6 +188,49 @@ int choose_splits(int64_t m_blocks, int64_t v_tiles, int sms, int64_t requested)
     return best;
 }
 
+cudaEvent_t pool_event(fce_handle h) {
+    if (!h->event_pool.empty()) {
+        cudaEvent_t e = h->event_pool.back();
+        h->event_pool.pop_back();
+        return e;
+    }
+    cudaEvent_t e = nullptr;
+    cudaEventCreate(&e);
+    return e;
+}
+
+// Launches one tile kernel; with timing on, brackets it with CUDA events on
+// the handle's stream and records its algorithmic flop count.
+cudaError_t timed_launch(fce_handle h, const TileParams& p, const TensorMaps& maps, double flops) {
+    cudaEvent_t e0 = nullptr, e1 = nullptr;
+    if (h->timing) {
+        e0 = pool_event(h);
+        e1 = pool_event(h);
+        cudaEventRecord(e0, h->stream);
+    }
+    cudaError_t e = launch_tile_kernel(p, maps, h->sms, h->stream);
+    if (h->timing) {
+        cudaEventRecord(e1, h->stream);
+        h->pending.push_back({p.mode, e0, e1, flops});
+    }
+    h->launches += 1;
+    return e;
+}
+
+void drain_timing(fce_handle h) {
+    for (auto& q : h->pending) {
+        cudaEventSynchronize(q.stop);
+        float ms = 0.f;
+        cudaEventElapsedTime(&ms, q.start, q.stop);
+        h->k_ms[q.mode] += ms;
+        h->k_flops[q.mode] += q.flops;
+        h->k_launches[q.mode] += 1;
+        h->event_pool.push_back(q.start);
+        h->event_pool.push_back(q.stop);
+    }
+    h->pending.clear();
+}
+
 fce_status run_forward_tiles(fce_handle h, const fce_problem* p, int splits, float* pm, float* pa,
                              float* pzt, uint8_t* pf) {
     TileParams tp;
@@ -200,9 +257,8 @@ fce_status run_forward_tiles(fce_handle h, const fce_problem* p, int splits, flo
     tp.part_a = pa;
     tp.part_zt = pzt;
     tp.part_found = pf;
-    cudaError_t e = launch_tile_kernel(tp, maps, h->sms, h->stream);
+    cudaError_t e = timed_launch(h, tp, maps, 2.0 * p->n * p->d * p->v);
     if (e != cudaSuccess) return fail(FCE_CUDA_ERROR, "forward tile kernel: %s", cudaGetErrorString(e));
-    h->launches += 1;
     return FCE_OK;
 }
 
@@ -272,6 +328,8 @@ fce_status fce_destroy(fce_handle h) {
     if (!h) return FCE_OK;
     cudaSetDevice(h->device);
     cudaStreamSynchronize(h->stream);
+    drain_timing(h);
+    for (cudaEvent_t e : h->event_pool) cudaEventDestroy(e);
     if (h->ws) cudaFree(h->ws);
     if (h->err) cudaFree(h->err);
     if (h->host_err) cudaFreeHost(h->host_err);
@@ -298,6 +356,10 @@ fce_status fce_set_option(fce_handle h, const char* key, int64_t value) {
         h->row_chunk = value;
     } else if (!std::strcmp(key, "validate")) {
         h->validate = value ? 1 : 0;
+    } else if (!std::strcmp(key, "timing")) {
+        drain_timing(h);
+        for (int i = 0; i < 3; ++i) h->k_ms[i] = h->k_flops[i] = 0, h->k_launches[i] = 0;
+        h->timing = value ? 1 : 0;
     } else {
         return fail(FCE_INVALID_ARGUMENT, "unknown option '%s'", key);
     }
@@ -308,6 +370,17 @@ fce_status fce_workspace_bytes(fce_handle h, size_t* current, size_t* peak) {
     if (!h) return fail(FCE_INVALID_ARGUMENT, "null handle");
     if (current) *current = h->ws_size + sizeof(int) * kErrSlots + 64;
     if (peak) *peak = h->ws_peak;
+    return FCE_OK;
+}
+
+fce_status fce_kernel_stats(fce_handle h, int kernel, double* total_ms, int64_t* launches,
+                            double* flops) {
+    if (!h) return fail(FCE_INVALID_ARGUMENT, "null handle");
+    if (kernel < 0 || kernel > 2) return fail(FCE_INVALID_ARGUMENT, "kernel id must be 0..2");
+    drain_timing(h);
+    if (total_ms) *total_ms = h->k_ms[kernel];
+    if (launches) *launches = h->k_launches[kernel];
+    if (flops) *flops = h->k_flops[kernel];
     return FCE_OK;
 }
 
@@ -506,9 +579,8 @@ fce_status fce_backward(fce_handle h, const fce_problem* p, fce_stats stats, int
             tp.gamma = gamma + r0;
             tp.g_out = G;
             tp.ldg = band;
-            e = launch_tile_kernel(tp, maps, h->sms, h->stream);
+            e = timed_launch(h, tp, maps, 2.0 * nc * p->d * vc);
             if (e != cudaSuccess) return fail(FCE_CUDA_ERROR, "grad tile kernel: %s", cudaGetErrorString(e));
-            h->launches += 1;
 
             // K2b + K2c in one persistent launch:
             //   prob 0: dW[vb:vb+vc] (+)= G^T . H[r0:r0+nc]   (A, B MN-major)
@@ -557,9 +629,8 @@ fce_status fce_backward(fce_handle h, const fce_problem* p, fce_stats stats, int
             gp.mode = kEpiGemm;
             gp.units0 = gp.prob[0].m_tiles * gp.prob[0].n_tiles;
             gp.units = gp.units0 + (np > 1 ? gp.prob[1].m_tiles * gp.prob[1].n_tiles : 0);
-            e = launch_tile_kernel(gp, gm, h->sms, h->stream);
+            e = timed_launch(h, gp, gm, 2.0 * nc * p->d * vc * np);
             if (e != cudaSuccess) return fail(FCE_CUDA_ERROR, "gemm tile kernel: %s", cudaGetErrorString(e));
-            h->launches += 1;
         }
     }
     return FCE_OK;

@@ -68,6 +68,8 @@ struct TensorMaps {
 
 // Stream a handle launches on (fce_api.cpp).
 cudaStream_t handle_stream(fce_handle h);
+// Thread-local message returned by fce_last_error (fce_api.cpp).
+void set_last_error(const char* msg);
 
 // Host helpers (fce_kernels.cu)
 bool encode_map_2d(CUtensorMap* map, const void* base, uint64_t inner, uint64_t outer,

@@ -72,15 +72,13 @@ NcclApi& nccl() {
     return api;
 }
 
-thread_local std::string g_vp_error;
-
 fce_status vp_fail(fce_status s, const char* fmt, ...) {
     char buf[512];
     va_list ap;
     va_start(ap, fmt);
     vsnprintf(buf, sizeof(buf), fmt, ap);
     va_end(ap);
-    g_vp_error = buf;
+    fce::set_last_error(buf);
     return s;
 }
 
@@ -97,7 +95,7 @@ struct fce_comm_s {
 
 extern "C" {
 
-const char* fce_vp_last_error(void) { return g_vp_error.c_str(); }
+const char* fce_vp_last_error(void) { return fce_last_error(); }
 
 fce_status fce_comm_unique_id(uint8_t* out, size_t len) {
     if (!out || len < sizeof(ncclUniqueId)) return vp_fail(FCE_INVALID_ARGUMENT, "id buffer too small");

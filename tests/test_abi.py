@@ -1,0 +1,82 @@
+"""CPU tests of the drop-in boundary: libfce.so loads and exports every symbol
+include/fce/*.h declares; status codes mirror the reference error taxonomy;
+without a GPU the library refuses to run (no CPU fallback)."""
+import ctypes
+import glob
+import os
+import re
+
+import pytest
+
+import paper_2511_17599_b200 as fce
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+# fusedce::ErrorCode declaration order, reference proj/include/fusedce/errors.hpp:10-21
+REFERENCE_ERROR_ORDER = ["DimensionMismatch", "TargetOutOfRange", "UnderflowRelease",
+                         "DuplicateTarget", "MissingStats", "InconsistentUpstream",
+                         "UnsupportedReduction", "InvalidLayout", "EmptyGrid", "EmptyInput"]
+
+
+def declared_symbols():
+    names = set()
+    for h in glob.glob(os.path.join(ROOT, "include", "fce", "*.h")):
+        text = open(h).read()
+        names |= set(re.findall(r"^\s*(?:fce_status|const char\*)\s+(fce_\w+)\s*\(", text, re.M))
+    return names
+
+
+def test_library_exports_every_declared_symbol():
+    lib = fce.load_library()
+    syms = declared_symbols()
+    assert len(syms) >= 20
+    missing = [s for s in sorted(syms) if not hasattr(lib, s)]
+    assert not missing, missing
+    assert syms == set(fce.EXPORTED_SYMBOLS)
+
+
+def test_status_codes_mirror_reference_error_order():
+    lib = fce.load_library()
+    for i, name in enumerate(REFERENCE_ERROR_ORDER):
+        assert lib.fce_status_string(i + 1).decode() == name
+        assert fce._STATUS[i + 1].__name__ == name
+    assert lib.fce_status_string(0).decode() == "ok"
+
+
+def test_null_handle_is_rejected():
+    lib = fce.load_library()
+    p = fce.FceProblem()
+    st = lib.fce_forward(None, ctypes.byref(p), 0, 0, fce.FceStats(), None, None, None)
+    assert st == 102  # FCE_INVALID_ARGUMENT
+
+
+def test_no_cpu_fallback_without_gpu():
+    import torch
+    if torch.cuda.is_available():
+        pytest.skip("GPU present")
+    lib = fce.load_library()
+    h = ctypes.c_void_p()
+    st = lib.fce_create(ctypes.byref(h), 0, None)
+    assert st == 100  # FCE_CUDA_ERROR: no device, and no CPU path
+    assert b"no CPU path" in lib.fce_last_error()
+
+
+def test_shard_ranges_ceil_first():
+    # ShardLayout::tensor_parallel / partition_ranges (parallel_sim.hpp:55-57, exec.hpp:25-41)
+    assert fce.shard_ranges(128256, 8) == [(i * 16032, (i + 1) * 16032) for i in range(8)]
+    assert [b - a for a, b in fce.shard_ranges(10, 4)] == [3, 3, 2, 2]
+    with pytest.raises(fce.InvalidLayout):
+        fce.shard_ranges(3, 4)
+    with pytest.raises(fce.InvalidLayout):
+        fce.shard_ranges(3, 0)
+
+
+def test_sass_is_tcgen05():
+    """The shipped kernels are tcgen05 / TMA (not mma.sync)."""
+    import shutil
+    import subprocess
+    if not shutil.which("cuobjdump"):
+        pytest.skip("cuobjdump absent")
+    out = subprocess.run(["cuobjdump", "-sass", fce.LIB_PATH], capture_output=True, text=True).stdout
+    assert "UTCHMMA" in out and "UTMALDG" in out and "LDTM" in out
+    assert not re.search(r"\bHMMA\b", out)

@@ -1,0 +1,445 @@
+"""GPU parity: the CUDA path (libfce.so through the C-ABI) against the CPU oracle
+and the reference-made golden fixtures, on the same seeded bf16-grid inputs.
+
+Tolerances (BASELINE.json north star): loss / lse within 1e-3 relative, dH / dW
+within 1e-2 relative max-norm (max|d| / max|ref|), target gather (found flags),
+ignore_index handling and N_valid exact.  Observed errors are far smaller
+(loss ~1e-7, grads ~1e-3: G is quantised to bf16 for the tensor cores).
+"""
+import glob
+import math
+import os
+
+import numpy as np
+import pytest
+import torch
+
+import paper_2511_17599_b200 as fce
+from oracle import bindings as ob
+
+pytestmark = pytest.mark.gpu
+
+GOLDEN = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden")
+LOSS_RTOL = 1e-3
+GRAD_RTOL = 1e-2
+
+
+def relmax(got, ref):
+    got = np.asarray(got, np.float64)
+    ref = np.asarray(ref, np.float64)
+    scale = np.abs(ref).max()
+    if scale == 0:
+        return float(np.abs(got).max())
+    return float(np.abs(got - ref).max() / scale)
+
+
+def to_dev(H, W, Y):
+    return (torch.from_numpy(np.ascontiguousarray(H)).cuda().to(torch.bfloat16),
+            torch.from_numpy(np.ascontiguousarray(W)).cuda().to(torch.bfloat16),
+            torch.from_numpy(np.ascontiguousarray(Y)).cuda())
+
+
+def check_forward(out, st, rows, lred, Y, ign, reduction):
+    m = out.stats.m.cpu().numpy()
+    a = out.stats.a.cpu().numpy()
+    zt = out.stats.z_target.cpu().numpy()
+    f = out.stats.found.cpu().numpy()
+    valid = np.ones(len(Y), bool) if ign is None else (Y != ign)
+    # target gather / ignore handling: exact
+    np.testing.assert_array_equal(f, st["found"])
+    assert np.all(np.isneginf(m[~valid])) and np.all(a[~valid] == 0) and np.all(zt[~valid] == 0)
+    got_rows = out.loss_rows.cpu().numpy()
+    assert np.all(got_rows[~valid] == 0.0)
+    # lse / loss: 1e-3 relative
+    lse_ref = (st["m"] + np.log(np.where(valid, st["a"], 1))).astype(np.float64)
+    lse = out.lse.cpu().numpy().astype(np.float64)
+    if valid.any():
+        assert np.max(np.abs(lse[valid] - lse_ref[valid]) / np.maximum(1.0, np.abs(lse_ref[valid]))) < LOSS_RTOL
+        assert np.max(np.abs(zt[valid] - st["z_target"][valid]) / np.maximum(1.0, np.abs(st["z_target"][valid]))) < LOSS_RTOL
+        assert np.max(np.abs(got_rows - rows) / np.maximum(1.0, np.abs(rows))) < LOSS_RTOL
+    if reduction != "none":
+        got = out.loss.item()
+        assert abs(got - lred) <= LOSS_RTOL * max(1.0, abs(lred)), (got, lred)
+
+
+def check_grads(dh, dw, dH_ref, dW_ref, Y, ign):
+    dh = dh.cpu().numpy()
+    dw = dw.cpu().numpy()
+    assert relmax(dh, dH_ref) < GRAD_RTOL
+    assert relmax(dw, dW_ref) < GRAD_RTOL
+    if ign is not None:
+        assert np.all(dh[Y == ign] == 0.0)  # ignored rows contribute exactly nothing
+
+
+# ------------------------------------------------------------------ generator
+
+def test_device_generator_is_bit_identical(cuda):
+    for (n, d, v, seed, frac) in [(37, 45, 301, 5, 0.3), (64, 512, 1000, 42, 0.0)]:
+        H, W, Y, Hf, Wf = fce.generate_instance(n, d, v, seed, -100, frac, want_f32=True)
+        Ho, Wo, Yo = ob.make_instance(n, d, v, seed, -100, frac)
+        np.testing.assert_array_equal(Hf.cpu().numpy(), Ho)
+        np.testing.assert_array_equal(Wf.cpu().numpy(), Wo)
+        np.testing.assert_array_equal(Y.cpu().numpy(), Yo)
+        np.testing.assert_array_equal(H.float().cpu().numpy(), Ho)  # bf16 cast is exact on the grid
+
+
+# ------------------------------------------------------------------ golden
+
+GOLDEN_CASES = sorted(os.path.basename(p)[:-4] for p in glob.glob(os.path.join(GOLDEN, "*.npz")))
+
+
+@pytest.mark.parametrize("case", GOLDEN_CASES)
+def test_golden_fixture(cuda, case):
+    g = dict(np.load(os.path.join(GOLDEN, case + ".npz")))
+    n, d, v = (int(x) for x in g["dims"])
+    H, W, Y = g["H"], g["W"], g["Y"]
+    if not W.size:
+        _, W, _ = ob.make_instance(n, d, v, int(g["seed"]), -100, 0.0)
+    ign = int(g["ignore_index"]) if int(g["has_ignore"]) else None
+    red = str(g["reduction"])
+    ranks = int(g["ranks"])
+    window = int(g["window"])
+    Hd, Wd, Yd = to_dev(H, W, Y)
+    st = np.zeros(n, ob.STATS_DTYPE)
+    st["m"], st["a"], st["z_target"], st["found"] = g["m"], g["a"], g["z_target"], g["found"]
+    if ranks == 1:
+        out = fce.fused_forward(Hd, Wd, Yd, red, ign, window=window)
+    else:
+        # simulated ranks on one GPU (the reference's own approach, parallel_sim.hpp:19-21)
+        parts = [fce.tp_rank_partial(Hd, Wd[lo:hi], lo, v, Yd, ign) for lo, hi in fce.shard_ranges(v, ranks)]
+        out = fce.merge_rank_partials(parts, Yd, red, ign)
+    check_forward(out, st, g["loss_rows"], float(g["loss_reduced"]), Y, ign, red)
+    up = torch.from_numpy(g["upstream"]).cuda() if red == "none" else 1.0
+    if ranks == 1:
+        dh, dw = fce.fused_backward_recompute(Hd, Wd, Yd, out.stats, red, up, ign)
+    else:
+        dh, dw = _tp_backward(Hd, Wd, Yd, out.stats, red, up, ign, ranks)
+    if g["dW"].size:
+        check_grads(dh, dw, g["dH"], g["dW"], Y, ign)
+    else:
+        assert relmax(dh.cpu().numpy(), g["dH"]) < GRAD_RTOL
+        assert relmax(dw[:64].cpu().numpy(), g["dW_head"]) < GRAD_RTOL
+        rs = dw.double().sum(1).cpu().numpy()
+        assert np.abs(rs - g["dW_rowsum"]).max() < GRAD_RTOL * np.abs(dw.cpu().numpy()).max() * d
+
+
+def _tp_backward(Hd, Wd, Yd, stats, red, up, ign, ranks):
+    """tp_backward (parallel_sim.hpp:246-290) with simulated ranks on one GPU:
+    each shard accumulates into dH, dW shards written in place."""
+    n, d = Hd.shape
+    v = Wd.shape[0]
+    dh = torch.zeros(n, d, dtype=torch.float32, device="cuda")
+    dw = torch.empty(v, d, dtype=torch.float32, device="cuda")
+    h = fce.default_handle(0)
+    import ctypes
+    for lo, hi in fce.shard_ranges(v, ranks):
+        p, keep = fce.make_problem(Hd, Wd[lo:hi], Yd, ign, lo, v)
+        up_rows = up if not isinstance(up, float) else None
+        fce._check(h.lib.fce_backward(h.raw, ctypes.byref(p), stats.c(), fce.REDUCTIONS[red],
+                                      0.0 if up_rows is not None else float(up),
+                                      fce._ptr(up_rows), dh.data_ptr(), d, dw[lo:hi].data_ptr(), d, 1))
+    return dh, dw
+
+
+# ------------------------------------------------------------------ random / ragged
+
+def _oracle_case(n, d, v, seed, frac, red, window=0):
+    H, W, Y = ob.make_instance(n, d, v, seed, -100, frac)
+    ign = -100 if frac > 0 else None
+    st, rows, lred = ob.forward(H, W, Y, red, ign, window)
+    return H, W, Y, ign, st, rows, lred
+
+
+@pytest.mark.parametrize("rep", range(10))
+def test_random_ragged_shapes(cuda, rep):
+    # shapes drawn like the reference verify suites (verify.cpp:88-90) plus tile edges
+    rng = np.random.default_rng(1000 + rep)
+    n = int(rng.integers(1, 300))
+    d = int(rng.integers(1, 200))
+    v = int(rng.integers(1, 1200))
+    frac = 0.25 if rep % 2 else 0.0
+    red = ("mean", "sum", "none")[rep % 3]
+    H, W, Y, ign, st, rows, lred = _oracle_case(n, d, v, 7 + rep, frac, red)
+    Hd, Wd, Yd = to_dev(H, W, Y)
+    out = fce.fused_forward(Hd, Wd, Yd, red, ign)
+    check_forward(out, st, rows, lred, Y, ign, red)
+    up = np.linspace(0.25, 2.0, n).astype(np.float32) if red == "none" else 1.0
+    dH, dW = ob.backward(H, W, Y, st, red, up, ign)
+    upd = torch.from_numpy(up).cuda() if red == "none" else 1.0
+    dh, dw = fce.fused_backward_recompute(Hd, Wd, Yd, out.stats, red, upd, ign)
+    check_grads(dh, dw, dH, dW, Y, ign)
+
+
+@pytest.mark.parametrize("shape", [(1, 1, 1), (1, 8, 1), (3, 1, 2), (128, 64, 256), (129, 64, 257),
+                                   (255, 72, 511), (256, 128, 513), (384, 4096, 300)])
+def test_tile_edges(cuda, shape):
+    n, d, v = shape
+    H, W, Y, ign, st, rows, lred = _oracle_case(n, d, v, 17, 0.0, "sum")
+    Hd, Wd, Yd = to_dev(H, W, Y)
+    out = fce.fused_forward(Hd, Wd, Yd, "sum")
+    check_forward(out, st, rows, lred, Y, ign, "sum")
+    if v == 1:
+        assert out.loss.item() == 0.0  # V = 1 -> loss 0 (test_fused_forward.cpp:266-273)
+    dH, dW = ob.backward(H, W, Y, st, "sum")
+    dh, dw = fce.fused_backward_recompute(Hd, Wd, Yd, out.stats, "sum")
+    check_grads(dh, dw, dH, dW, Y, ign)
+
+
+def test_small_config(cuda):
+    """BASELINE configs[0]: N=256, D=512, V=32000, seed 42, mean."""
+    H, W, Y, ign, st, rows, lred = _oracle_case(256, 512, 32000, 42, 0.0, "mean")
+    Hd, Wd, Yd = to_dev(H, W, Y)
+    out = fce.fused_forward(Hd, Wd, Yd, "mean")
+    check_forward(out, st, rows, lred, Y, ign, "mean")
+    dH, dW = ob.backward(H, W, Y, st, "mean")
+    dh, dw = fce.fused_backward_recompute(Hd, Wd, Yd, out.stats, "mean")
+    check_grads(dh, dw, dH, dW, Y, ign)
+
+
+def test_small_config_with_backward_chunking(cuda):
+    """Multiple row chunks x vocab bands (dW accumulation across row chunks)."""
+    H, W, Y, ign, st, rows, lred = _oracle_case(700, 136, 3000, 5, 0.25, "mean")
+    Hd, Wd, Yd = to_dev(H, W, Y)
+    h = fce.Handle(0)
+    h.set_option("row_chunk", 256)
+    h.set_option("band_cols", 512)
+    out = fce.fused_forward(Hd, Wd, Yd, "mean", ign, handle=h)
+    check_forward(out, st, rows, lred, Y, ign, "mean")
+    dH, dW = ob.backward(H, W, Y, st, "mean", 1.0, ign)
+    dh, dw = fce.fused_backward_recompute(Hd, Wd, Yd, out.stats, "mean", 1.0, ign, handle=h)
+    check_grads(dh, dw, dH, dW, Y, ign)
+    h.close()
+
+
+@pytest.mark.parametrize("window", [1, 3, 16, 128, 256, 257, 1000])
+def test_windowed_forward(cuda, window):
+    # window sweep {1,3,16,128,256,257} (test_fused_forward.cpp:146-175)
+    H, W, Y, ign, st, rows, lred = _oracle_case(70, 48, 700, 23, 0.2, "mean")
+    st_w, rows_w, lred_w = ob.forward(H, W, Y, "mean", ign, window)
+    Hd, Wd, Yd = to_dev(H, W, Y)
+    out = fce.fused_forward_windowed(Hd, Wd, Yd, window, "mean", ign)
+    check_forward(out, st_w, rows_w, lred_w, Y, ign, "mean")
+
+
+@pytest.mark.parametrize("splits", [1, 2, 5, 64])
+def test_split_invariance(cuda, splits):
+    H, W, Y, ign, st, rows, lred = _oracle_case(300, 64, 5000, 31, 0.0, "mean")
+    Hd, Wd, Yd = to_dev(H, W, Y)
+    h = fce.Handle(0)
+    h.set_option("splits", splits)
+    out = fce.fused_forward(Hd, Wd, Yd, "mean", handle=h)
+    check_forward(out, st, rows, lred, Y, ign, "mean")
+    h.close()
+
+
+# ------------------------------------------------------------------ numerics
+
+def test_peaked_logits_target_gather(cuda):
+    """H scaled so the logit std is ~3: a wrong target gather moves the loss by O(1)
+    (with the reference distribution a wrong gather hides below 1e-3)."""
+    H, W, Y = ob.make_instance(200, 64, 2000, 77)
+    H = np.vectorize(ob.oracle_lib().orc_round_bf16, otypes=[np.float32])(H * 24.0)
+    st, rows, lred = ob.forward(H, W, Y, "none")
+    assert rows.std() > 1.0
+    Hd, Wd, Yd = to_dev(H, W, Y)
+    out = fce.fused_forward(Hd, Wd, Yd, "none")
+    check_forward(out, st, rows, lred, Y, None, "none")
+    dH, dW = ob.backward(H, W, Y, st, "none", np.ones(200, np.float32))
+    dh, dw = fce.fused_backward_recompute(Hd, Wd, Yd, out.stats, "none", torch.ones(200, device="cuda"))
+    check_grads(dh, dw, dH, dW, Y, None)
+
+
+def test_large_offset_stability(cuda):
+    """+10240 shared logit offset (bf16 variant of verify.cpp:422-492 /
+    acceptance_test.cpp:336-402): finite and equal to the unshifted loss within 1e-4."""
+    n, dq, v = 8, 8, 32
+    d = dq + 1
+    st_ = np.array([0x57AB1E], np.uint64)
+    lib = ob.oracle_lib()
+    import ctypes
+    state = ctypes.c_uint64(0x57AB1E)
+
+    def quarter():
+        return (float(lib.orc_splitmix64(ctypes.byref(state)) % 9) - 4.0) / 4.0
+
+    H = np.zeros((n, d), np.float32)
+    Wb = np.zeros((v, d), np.float32)
+    for i in range(n):
+        for k in range(dq):
+            H[i, k] = quarter()
+        H[i, dq] = 1.0
+    for r in range(v):
+        for k in range(dq):
+            Wb[r, k] = quarter()
+    Ws = Wb.copy()
+    Ws[:, dq] = 10240.0
+    Y = np.array([lib.orc_splitmix64(ctypes.byref(state)) % v for _ in range(n)], np.int64)
+    _, rows_base, _ = ob.forward(H, Wb, Y, "none")
+    Hd, Wd, Yd = to_dev(H, Ws, Y)
+    out = fce.fused_forward(Hd, Wd, Yd, "none")
+    got = out.loss_rows.cpu().numpy()
+    assert np.all(np.isfinite(got))
+    assert np.max(np.abs(got - rows_base) / np.maximum(1e-30, np.abs(rows_base))) <= 1e-4
+    assert np.all(out.stats.m.cpu().numpy() > 10000)
+
+
+def test_all_ignored_mean_is_zero_with_zero_grads(cuda):
+    # test_reference.cpp:111-130
+    H, W, _ = ob.make_instance(40, 16, 100, 11)
+    Y = np.full(40, -100, np.int64)
+    Hd, Wd, Yd = to_dev(H, W, Y)
+    out = fce.fused_forward(Hd, Wd, Yd, "mean", -100)
+    assert out.loss.item() == 0.0
+    dh, dw = fce.fused_backward_recompute(Hd, Wd, Yd, out.stats, "mean", 1.0, -100)
+    assert torch.count_nonzero(dh).item() == 0 and torch.count_nonzero(dw).item() == 0
+
+
+def test_zero_upstream_gives_exact_zeros(cuda):
+    # test_fused_backward.cpp:151-162
+    H, W, Y = ob.make_instance(50, 24, 300, 4)
+    Hd, Wd, Yd = to_dev(H, W, Y)
+    out = fce.fused_forward(Hd, Wd, Yd, "sum")
+    dh, dw = fce.fused_backward_recompute(Hd, Wd, Yd, out.stats, "sum", 0.0)
+    assert torch.count_nonzero(dh).item() == 0 and torch.count_nonzero(dw).item() == 0
+
+
+def test_upstream_linearity_is_exact(cuda):
+    # test_fused_backward.cpp:306-321; scaling by 2 is exact through the bf16 G
+    H, W, Y = ob.make_instance(90, 40, 700, 8)
+    Hd, Wd, Yd = to_dev(H, W, Y)
+    out = fce.fused_forward(Hd, Wd, Yd, "sum")
+    dh1, dw1 = fce.fused_backward_recompute(Hd, Wd, Yd, out.stats, "sum", 1.0)
+    dh2, dw2 = fce.fused_backward_recompute(Hd, Wd, Yd, out.stats, "sum", 2.0)
+    assert torch.equal(dh2, 2 * dh1) and torch.equal(dw2, 2 * dw1)
+
+
+def test_ignored_row_equals_dropped_row(cuda):
+    # test_fused_backward.cpp:212-245: an ignored row is the same as the row not existing
+    H, W, Y = ob.make_instance(60, 32, 400, 21)
+    Yi = Y.copy()
+    Yi[::3] = -100
+    keep = Yi != -100
+    Hd, Wd, Yd = to_dev(H, W, Yi)
+    out = fce.fused_forward(Hd, Wd, Yd, "sum", -100)
+    dh, dw = fce.fused_backward_recompute(Hd, Wd, Yd, out.stats, "sum", 1.0, -100)
+    Hk, Wk, Yk = to_dev(H[keep], W, Y[keep])
+    outk = fce.fused_forward(Hk, Wk, Yk, "sum")
+    dhk, dwk = fce.fused_backward_recompute(Hk, Wk, Yk, outk.stats, "sum")
+    assert abs(out.loss.item() - outk.loss.item()) <= 1e-5 * abs(outk.loss.item())
+    assert relmax(dw.cpu().numpy(), dwk.cpu().numpy()) < 1e-5
+    assert torch.count_nonzero(dh[torch.from_numpy(~keep).cuda()]).item() == 0
+
+
+def test_partial_grads_path_matches_recompute(cuda):
+    # Alg. 3/4 (fused_backward.hpp:162-202) == fused_backward_recompute
+    H, W, Y = ob.make_instance(80, 48, 600, 13, -100, 0.25)
+    Hd, Wd, Yd = to_dev(H, W, Y)
+    out, partials = fce.fused_forward_with_partial_grads(Hd, Wd, Yd, "mean", -100)
+    valid = int((Y != -100).sum())
+    dh_s, dw_s = fce.scale_partial_grads(partials, 1.0 / valid)
+    dh, dw = fce.fused_backward_recompute(Hd, Wd, Yd, out.stats, "mean", 1.0, -100)
+    assert relmax(dh_s.cpu().numpy(), dh.cpu().numpy()) < 1e-6
+    assert relmax(dw_s.cpu().numpy(), dw.cpu().numpy()) < 1e-6
+    with pytest.raises(fce.UnsupportedReduction):
+        fce.fused_forward_with_partial_grads(Hd, Wd, Yd, "none", -100)
+
+
+# ------------------------------------------------------------------ errors
+
+def test_error_taxonomy(cuda):
+    H, W, Y = ob.make_instance(16, 8, 10, 1)
+    Hd, Wd, Yd = to_dev(H, W, Y)
+    bad = Yd.clone()
+    bad[3] = 10
+    with pytest.raises(fce.TargetOutOfRange):
+        fce.fused_forward(Hd, Wd, bad, "mean")
+    bad[3] = -7  # negative, not the ignore sentinel
+    with pytest.raises(fce.TargetOutOfRange):
+        fce.fused_forward(Hd, Wd, bad, "mean", -100)
+    out = fce.fused_forward(Hd, Wd, Yd, "mean")
+    broken = fce.Stats(out.stats.m, out.stats.a, out.stats.z_target, out.stats.found.clone())
+    broken.found[2] = 0
+    with pytest.raises(fce.MissingStats):
+        fce.fused_backward_recompute(Hd, Wd, Yd, broken, "mean")
+    with pytest.raises(fce.InconsistentUpstream):
+        fce.fused_backward_recompute(Hd, Wd, Yd, out.stats, "none", 1.0)
+    with pytest.raises(fce.InconsistentUpstream):
+        fce.fused_backward_recompute(Hd, Wd, Yd, out.stats, "mean", torch.ones(16, device="cuda"))
+    with pytest.raises(fce.DimensionMismatch):
+        fce.fused_forward(Hd, Wd[:, :4], Yd, "mean")
+    with pytest.raises(fce.DimensionMismatch):
+        fce.fused_forward(Hd, Wd, Yd[:5], "mean")
+    with pytest.raises(fce.InvalidLayout):
+        fce.fused_forward_windowed(Hd, Wd, Yd, 0)
+    # duplicate target across overlapping "ranks"
+    p0 = fce.tp_rank_partial(Hd, Wd, 0, 10, Yd)
+    with pytest.raises(fce.DuplicateTarget):
+        fce.merge_rank_partials([p0, p0], Yd)
+
+
+# ------------------------------------------------------------------ vocab parallel
+
+@pytest.mark.parametrize("ranks", [2, 3, 8])
+def test_simulated_vocab_parallel(cuda, ranks):
+    """tp_forward / tp_backward semantics with per-shard launches on one GPU."""
+    H, W, Y, ign, st, rows, lred = _oracle_case(150, 64, 2001, 3, 0.25, "mean")
+    Hd, Wd, Yd = to_dev(H, W, Y)
+    v = W.shape[0]
+    parts = [fce.tp_rank_partial(Hd, Wd[lo:hi], lo, v, Yd, ign) for lo, hi in fce.shard_ranges(v, ranks)]
+    # exactly-once target capture (test_parallel_sim.cpp:77-96)
+    found = torch.stack([p.found for p in parts]).sum(0).cpu().numpy()
+    np.testing.assert_array_equal(found, (Y != -100).astype(np.uint8))
+    out = fce.merge_rank_partials(parts, Yd, "mean", ign)
+    check_forward(out, st, rows, lred, Y, ign, "mean")
+    dH, dW = ob.backward(H, W, Y, st, "mean", 1.0, ign)
+    dh, dw = _tp_backward(Hd, Wd, Yd, out.stats, "mean", 1.0, ign, ranks)
+    check_grads(dh, dw, dH, dW, Y, ign)
+
+
+def test_native_vocab_parallel_single_rank(cuda):
+    """fce_vp_forward / fce_vp_backward over a 1-rank NCCL communicator."""
+    import ctypes
+    from paper_2511_17599_b200 import vocab_parallel as vp
+    H, W, Y, ign, st, rows, lred = _oracle_case(100, 32, 900, 9, 0.0, "mean")
+    Hd, Wd, Yd = to_dev(H, W, Y)
+    comm = vp.NativeComm.create_local(device=0)
+    out = vp.native_forward(comm, Hd, Wd, Yd, 0, 900, "mean")
+    check_forward(out, st, rows, lred, Y, ign, "mean")
+    dH, dW = ob.backward(H, W, Y, st, "mean")
+    dh, dw = vp.native_backward(comm, Hd, Wd, Yd, 0, 900, out.stats, "mean")
+    check_grads(dh, dw, dH, dW, Y, ign)
+    comm.close()
+
+
+# ------------------------------------------------------------------ full size
+
+@pytest.mark.slow
+def test_llama3_8b_shape_properties(cuda):
+    """BASELINE configs[1] at full size (N=16384, D=4096, V=128256): a row slice
+    against the oracle, plus size-independent properties of the whole result."""
+    n, d, v = 16384, 4096, 128256
+    Hd, Wd, Yd = fce.generate_instance(n, d, v, 42)
+    out = fce.fused_forward(Hd, Wd, Yd, "sum")
+    assert torch.all(out.stats.found == 1)
+    lse = out.lse
+    assert torch.isfinite(lse).all()
+    assert abs(out.loss.item() / n - math.log(v)) < 0.05  # ~uniform logits
+    # row slice vs oracle at full D, V (rows are independent)
+    rows_idx = [0, 1, 4097, 16383]
+    Hs = Hd[rows_idx].float().cpu().numpy()
+    Ys = Yd[rows_idx].cpu().numpy()
+    Wn = Wd.float().cpu().numpy()
+    st, rows, _ = ob.forward(Hs, Wn, Ys, "none")
+    np.testing.assert_array_equal(out.stats.found[rows_idx].cpu().numpy(), st["found"])
+    got = out.loss_rows[rows_idx].cpu().numpy()
+    assert np.max(np.abs(got - rows) / np.abs(rows)) < LOSS_RTOL
+    dh, dw = fce.fused_backward_recompute(Hd, Wd, Yd, out.stats, "sum", 1.0)
+    # dH rows depend only on their own row: compare the slice to the oracle
+    dH_ref, _ = ob.backward(Hs, Wn, Ys, st, "sum", 1.0, want_dw=False)
+    assert relmax(dh[rows_idx].cpu().numpy(), dH_ref) < GRAD_RTOL
+    # sum_v G[n, v] = 0 per row => dW columns sum to ~0 (test_reference.cpp:218-233)
+    col = dw.double().sum(0)
+    assert col.abs().max().item() < 1e-3 * dw.abs().max().item() * math.sqrt(v)
+    # linearity: upstream 2 doubles both gradients exactly
+    dh2, dw2 = fce.fused_backward_recompute(Hd, Wd, Yd, out.stats, "sum", 2.0)
+    assert torch.equal(dh2, 2 * dh) and torch.equal(dw2, 2 * dw)
