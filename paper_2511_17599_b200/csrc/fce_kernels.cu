@@ -281,8 +281,10 @@ __global__ void __launch_bounds__(kThreads, 1)
                             }
                             a_run += s0 + s1;
                         }
+                        // target capture only inside this launch's valid columns: a
+                        // shard's padded tail must not claim a neighbour's target
                         const int64_t tc = tcol - col0;
-                        if (tc >= 0 && tc < 32) {
+                        if (tc >= 0 && tc < 32 && col0 + tc < p.v_cols) {
 #pragma unroll
                             for (int j = 0; j < 32; ++j)
                                 if (j == tc) zt = v[j];

@@ -337,9 +337,14 @@ def test_partial_grads_path_matches_recompute(cuda):
     out, partials = fce.fused_forward_with_partial_grads(Hd, Wd, Yd, "mean", -100)
     valid = int((Y != -100).sum())
     dh_s, dw_s = fce.scale_partial_grads(partials, 1.0 / valid)
+    st, _, _ = ob.forward(H, W, Y, "mean", -100)
+    dH, dW = ob.backward(H, W, Y, st, "mean", 1.0, -100)
+    # both device paths within the gradient tolerance of the oracle; they differ
+    # from each other only by where gamma enters the bf16 rounding of G
+    check_grads(dh_s, dw_s, dH, dW, Y, -100)
     dh, dw = fce.fused_backward_recompute(Hd, Wd, Yd, out.stats, "mean", 1.0, -100)
-    assert relmax(dh_s.cpu().numpy(), dh.cpu().numpy()) < 1e-6
-    assert relmax(dw_s.cpu().numpy(), dw.cpu().numpy()) < 1e-6
+    check_grads(dh, dw, dH, dW, Y, -100)
+    assert relmax(dh_s.cpu().numpy(), dh.cpu().numpy()) < 1e-2
     with pytest.raises(fce.UnsupportedReduction):
         fce.fused_forward_with_partial_grads(Hd, Wd, Yd, "none", -100)
 
