@@ -238,9 +238,9 @@ def test_peaked_logits_target_gather(cuda):
     """H scaled so the logit std is ~3: a wrong target gather moves the loss by O(1)
     (with the reference distribution a wrong gather hides below 1e-3)."""
     H, W, Y = ob.make_instance(200, 64, 2000, 77)
-    H = np.vectorize(ob.oracle_lib().orc_round_bf16, otypes=[np.float32])(H * 24.0)
+    H = np.vectorize(ob.oracle_lib().orc_round_bf16, otypes=[np.float32])(H * 48.0)
     st, rows, lred = ob.forward(H, W, Y, "none")
-    assert rows.std() > 1.0
+    assert rows.max() - rows.min() > 3.0  # strongly peaked: per-row losses spread by O(1)
     Hd, Wd, Yd = to_dev(H, W, Y)
     out = fce.fused_forward(Hd, Wd, Yd, "none")
     check_forward(out, st, rows, lred, Y, None, "none")
