@@ -277,7 +277,7 @@ def main():
     barrier()
     clk = clocks.stop()
     ms = e0.elapsed_time(e1)
-    kstats = {k: h.kernel_stats(k) for k in (0, 1, 2)}
+    kstats = {k: h.kernel_stats(k) for k in (0, 1, 2, 3)}
     h.set_option("timing", 0)
     launches = h.launch_count() - launches0
     t = torch.tensor([ms], device=dev)
@@ -343,7 +343,8 @@ def main():
     flops_step = 8.0 * n * d * v
     # dominant kernel by device time inside the timed region
     names = {0: "fce_fwd_sm100 (forward, online-LSE epilogue)", 1: "fce_bwd_grad_sm100 (recompute S, G=softmax-onehot)",
-             2: "fce_bwd_gemm_sm100 (dW=G^T.H and dH+=G.W)"}
+             2: "fce_bwd_gemm_sm100 (dW=G^T.H and dH+=G.W)",
+             3: "fce_bwd_persistent_sm100 (recompute S -> G -> dH, dW; one launch)"}
     dom = max(kstats, key=lambda k: kstats[k][0])
     kms, kl, kfl = kstats[dom]
     per_launch_ms = kms / max(kl, 1)

@@ -91,7 +91,8 @@ fce_status fce_set_stream(fce_handle h, void* stream);
 const char* fce_last_error(void);
 const char* fce_status_string(fce_status s);
 /* Tuning / behaviour knobs: "splits" (forward split-V factor, 0 = auto),
- * "band_cols" / "row_chunk" (backward G chunk, 0 = auto), "validate"
+ * "band_cols" / "row_chunk" (backward G chunk, 0 = auto), "bwd_persistent"
+ * (1 = one persistent backward launch, default; 0 = two launches per chunk), "validate"
  * (1 = sync and check targets / stats, default 1), "timing" (1 = per-kernel
  * event timing, see fce_kernel_stats; setting it resets the counters). */
 fce_status fce_set_option(fce_handle h, const char* key, int64_t value);
@@ -103,7 +104,7 @@ fce_status fce_launch_count(fce_handle h, int64_t* count);
 /* With option "timing" = 1 every tile-kernel launch is bracketed by CUDA
  * events on the handle's stream.  kernel: 0 = forward (online-LSE epilogue),
  * 1 = gradient producer (recompute + softmax - onehot), 2 = dW / dH
- * contractions.  Returns summed device time, launch count and algorithmic
+ * contractions (per-band path), 3 = persistent fused backward (default).  Returns summed device time, launch count and algorithmic
  * flops (2 * M * N * K per contraction) since timing was (re)enabled. */
 fce_status fce_kernel_stats(fce_handle h, int kernel, double* total_ms, int64_t* launches,
                             double* flops);

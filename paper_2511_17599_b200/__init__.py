@@ -174,7 +174,8 @@ class Handle:
         _check(self.lib.fce_launch_count(self._h, ctypes.byref(c)))
         return c.value
 
-    KERNELS = {0: "fce_fwd_sm100", 1: "fce_bwd_grad_sm100", 2: "fce_bwd_gemm_sm100"}
+    KERNELS = {0: "fce_fwd_sm100", 1: "fce_bwd_grad_sm100", 2: "fce_bwd_gemm_sm100",
+               3: "fce_bwd_persistent_sm100"}
 
     def kernel_stats(self, kernel: int):
         """(total device ms, launches, algorithmic flops) since timing was enabled."""

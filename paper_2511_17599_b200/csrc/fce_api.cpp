@@ -52,8 +52,9 @@ struct fce_handle_s {
     int* err = nullptr;                     // kErrSlots ints
     unsigned long long* count = nullptr;    // valid-target count
     int* host_err = nullptr;                // pinned mirror
-    int64_t splits = 0, band_cols = 0, row_chunk = 0, validate = 1;
+    int64_t splits = 0, band_cols = 0, row_chunk = 0, validate = 1, bwd_persistent = 1;
     int64_t launches = 0;
+    size_t bwd_scratch[4] = {0, 0, 0, 0};  // offsets of the persistent-backward scratch
     // optional per-kernel CUDA-event timing of the tile kernels (bench roofline)
     int64_t timing = 0;
     struct Pending {
@@ -63,9 +64,9 @@ struct fce_handle_s {
     };
     std::vector<Pending> pending;
     std::vector<cudaEvent_t> event_pool;
-    double k_ms[3] = {0, 0, 0};
-    double k_flops[3] = {0, 0, 0};
-    int64_t k_launches[3] = {0, 0, 0};
+    double k_ms[4] = {0, 0, 0, 0};
+    double k_flops[4] = {0, 0, 0, 0};
+    int64_t k_launches[4] = {0, 0, 0, 0};
 };
 
 namespace fce {
@@ -262,6 +263,111 @@ fce_status run_forward_tiles(fce_handle h, const fce_problem* p, int splits, flo
     return FCE_OK;
 }
 
+// Persistent backward: one launch of fce_bwd_persistent_kernel over every
+// (row chunk x vocab band) chunk; see fce_bwd.cu for the schedule.
+fce_status run_backward_persistent(fce_handle h, const fce_problem* p, const float* gamma,
+                                   const float* lse, int64_t row_chunk, int64_t band,
+                                   float* dhidden, int64_t lddh, float* dweight, int64_t lddw,
+                                   int accumulate_dhidden) {
+    char* ws = static_cast<char*>(h->ws);
+    __nv_bfloat16* g_ring = reinterpret_cast<__nv_bfloat16*>(ws + h->bwd_scratch[0]);
+    BwdChunk* d_tab = reinterpret_cast<BwdChunk*>(ws + h->bwd_scratch[1]);
+    int* d_bnd = reinterpret_cast<int*>(ws + h->bwd_scratch[2]);
+    unsigned* d_ctr = reinterpret_cast<unsigned*>(ws + h->bwd_scratch[3]);
+
+    const int64_t n_rc = ceil_div(p->n, row_chunk), n_bd = ceil_div(p->v, band);
+    const int64_t n_chunks = n_rc * n_bd;
+    const int mb_max = static_cast<int>(ceil_div(row_chunk, kBM));
+    const int d_tiles = static_cast<int>(ceil_div(p->d, kBN));
+    std::vector<BwdChunk> tab(n_chunks);
+    std::vector<int> bnd(2 * n_chunks + 1);
+    int64_t u = 0;
+    for (int64_t c = 0; c < n_chunks; ++c) {
+        BwdChunk& k = tab[c];
+        const int64_t ri = c / n_bd, bi = c % n_bd;
+        k.r0 = static_cast<int>(ri * row_chunk);
+        k.nc = static_cast<int>(std::min(row_chunk, p->n - ri * row_chunk));
+        k.vb = static_cast<int>(bi * band);
+        k.vc = static_cast<int>(std::min(band, p->v - bi * band));
+        k.slot = static_cast<int>(c & 1);
+        k.row_idx = static_cast<int>(ri);
+        k.band_idx = static_cast<int>(bi);
+        k.vt = static_cast<int>(ceil_div(k.vc, kBN));
+        k.vm = static_cast<int>(ceil_div(k.vc, kBM));
+        const int mbs = static_cast<int>(ceil_div(k.nc, kBM));
+        k.n_g = mbs * k.vt;
+        k.n_dh = dhidden ? mbs * d_tiles : 0;
+        k.n_dw = dweight ? k.vm * d_tiles : 0;
+        bnd[2 * c] = static_cast<int>(u);
+        u += k.n_g;
+        bnd[2 * c + 1] = static_cast<int>(u);
+        u += k.n_dh + k.n_dw;
+    }
+    bnd[2 * n_chunks] = static_cast<int>(u);
+    if (u >= INT32_MAX) return fail(FCE_INVALID_LAYOUT, "too many backward work units");
+    FCE_CUDA(cudaMemcpyAsync(d_tab, tab.data(), sizeof(BwdChunk) * n_chunks, cudaMemcpyHostToDevice, h->stream));
+    FCE_CUDA(cudaMemcpyAsync(d_bnd, bnd.data(), sizeof(int) * bnd.size(), cudaMemcpyHostToDevice, h->stream));
+    FCE_CUDA(cudaMemsetAsync(d_ctr, 0, sizeof(unsigned) * (1 + 4 * n_chunks + n_chunks * mb_max), h->stream));
+    // stale ring rows past a short last chunk are read (then masked or
+    // multiplied by zero-filled operands): keep them finite
+    FCE_CUDA(cudaMemsetAsync(g_ring, 0, sizeof(__nv_bfloat16) * 2 * row_chunk * band, h->stream));
+
+    BwdMaps maps;
+    std::memset(&maps, 0, sizeof(maps));
+    const uint64_t ring_rows = static_cast<uint64_t>(2 * row_chunk);
+    if (!encode_map_2d(&maps.h_k, p->hidden, p->d, p->n, p->ldh * 2, kBK, kBM) ||
+        !encode_map_2d(&maps.w_k, p->weight, p->d, p->v, p->ldw * 2, kBK, kBN) ||
+        !encode_map_2d(&maps.g_k, g_ring, band, ring_rows, band * 2, kBK, kBM) ||
+        !encode_map_2d(&maps.w_mn, p->weight, p->d, p->v, p->ldw * 2, 64, 64) ||
+        !encode_map_2d(&maps.g_mn, g_ring, band, ring_rows, band * 2, 64, 64) ||
+        !encode_map_2d(&maps.h_mn, p->hidden, p->d, p->n, p->ldh * 2, 64, 64))
+        return fail(FCE_CUDA_ERROR, "cuTensorMapEncodeTiled failed (persistent backward)");
+
+    BwdParams bp;
+    std::memset(&bp, 0, sizeof(bp));
+    bp.units = static_cast<int>(u);
+    bp.n_chunks = static_cast<int>(n_chunks);
+    bp.bands = static_cast<int>(n_bd);
+    bp.d_tiles = d_tiles;
+    bp.k_blocks_d = static_cast<int>(ceil_div(p->d, kBK));
+    bp.mb_max = mb_max;
+    bp.gm_base = static_cast<int>(1 + 4 * n_chunks);
+    bp.has_ignore = p->has_ignore;
+    bp.accumulate_dh = accumulate_dhidden;
+    bp.nc_max = row_chunk;
+    bp.ldg = band;
+    bp.d = p->d;
+    bp.lddh = lddh;
+    bp.lddw = lddw;
+    bp.v_offset = p->v_offset;
+    bp.ignore_index = p->ignore_index;
+    bp.chunks = d_tab;
+    bp.bnd = d_bnd;
+    bp.counters = d_ctr;
+    bp.targets = p->targets;
+    bp.lse = lse;
+    bp.gamma = gamma;
+    bp.g_ring = g_ring;
+    bp.dh = dhidden;
+    bp.dw = dweight;
+
+    cudaEvent_t e0 = nullptr, e1 = nullptr;
+    if (h->timing) {
+        e0 = pool_event(h);
+        e1 = pool_event(h);
+        cudaEventRecord(e0, h->stream);
+    }
+    cudaError_t e = launch_bwd_persistent(bp, maps, h->sms, h->stream);
+    if (h->timing) {
+        cudaEventRecord(e1, h->stream);
+        const double flops = 2.0 * p->n * p->d * p->v * (1 + (dhidden ? 1 : 0) + (dweight ? 1 : 0));
+        h->pending.push_back({3, e0, e1, flops});
+    }
+    h->launches += 1;
+    if (e != cudaSuccess) return fail(FCE_CUDA_ERROR, "persistent backward kernel: %s", cudaGetErrorString(e));
+    return FCE_OK;
+}
+
 }  // namespace
 
 extern "C" {
@@ -356,9 +462,11 @@ fce_status fce_set_option(fce_handle h, const char* key, int64_t value) {
         h->row_chunk = value;
     } else if (!std::strcmp(key, "validate")) {
         h->validate = value ? 1 : 0;
+    } else if (!std::strcmp(key, "bwd_persistent")) {
+        h->bwd_persistent = value ? 1 : 0;
     } else if (!std::strcmp(key, "timing")) {
         drain_timing(h);
-        for (int i = 0; i < 3; ++i) h->k_ms[i] = h->k_flops[i] = 0, h->k_launches[i] = 0;
+        for (int i = 0; i < 4; ++i) h->k_ms[i] = h->k_flops[i] = 0, h->k_launches[i] = 0;
         h->timing = value ? 1 : 0;
     } else {
         return fail(FCE_INVALID_ARGUMENT, "unknown option '%s'", key);
@@ -376,7 +484,7 @@ fce_status fce_workspace_bytes(fce_handle h, size_t* current, size_t* peak) {
 fce_status fce_kernel_stats(fce_handle h, int kernel, double* total_ms, int64_t* launches,
                             double* flops) {
     if (!h) return fail(FCE_INVALID_ARGUMENT, "null handle");
-    if (kernel < 0 || kernel > 2) return fail(FCE_INVALID_ARGUMENT, "kernel id must be 0..2");
+    if (kernel < 0 || kernel > 3) return fail(FCE_INVALID_ARGUMENT, "kernel id must be 0..3");
     drain_timing(h);
     if (total_ms) *total_ms = h->k_ms[kernel];
     if (launches) *launches = h->k_launches[kernel];
@@ -531,8 +639,18 @@ fce_status fce_backward(fce_handle h, const fce_problem* p, fce_stats stats, int
     Scratch sc(h);
     const size_t o_g = sc.take(sizeof(float) * p->n);
     const size_t o_l = sc.take(sizeof(float) * p->n);
-    const size_t o_G = sc.take(sizeof(__nv_bfloat16) * row_chunk * band);
+    const size_t o_G = sc.take(sizeof(__nv_bfloat16) * row_chunk * band * (h->bwd_persistent ? 2 : 1));
+    const int64_t n_rc = ceil_div(p->n, row_chunk), n_bd = ceil_div(p->v, band);
+    const int64_t n_chunks = n_rc * n_bd;
+    const int64_t mb_max = ceil_div(row_chunk, kBM);
+    const size_t o_tab = sc.take(sizeof(BwdChunk) * n_chunks);
+    const size_t o_bnd = sc.take(sizeof(int) * (2 * n_chunks + 1));
+    const size_t o_ctr = sc.take(sizeof(unsigned) * (1 + 4 * n_chunks + n_chunks * mb_max));
     if ((s = sc.commit())) return s;
+    h->bwd_scratch[0] = o_G;
+    h->bwd_scratch[1] = o_tab;
+    h->bwd_scratch[2] = o_bnd;
+    h->bwd_scratch[3] = o_ctr;
     float* gamma = sc.ptr<float>(o_g);
     float* lse = sc.ptr<float>(o_l);
     __nv_bfloat16* G = sc.ptr<__nv_bfloat16>(o_G);
@@ -547,6 +665,10 @@ fce_status fce_backward(fce_handle h, const fce_problem* p, fce_stats stats, int
     h->launches += 2;
     if ((s = read_errors(h, h->validate != 0))) return s;
     if (!dhidden && !dweight) return FCE_OK;
+
+    if (h->bwd_persistent)
+        return run_backward_persistent(h, p, gamma, lse, row_chunk, band, dhidden, lddh, dweight,
+                                       lddw, accumulate_dhidden);
 
     const int k_blocks_d = static_cast<int>(ceil_div(p->d, kBK));
     for (int64_t r0 = 0; r0 < p->n; r0 += row_chunk) {

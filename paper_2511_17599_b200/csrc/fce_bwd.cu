@@ -1,0 +1,445 @@
+// Persistent fused backward (one launch per fce_backward call).
+//
+// The backward of the reference (fused_backward_recompute,
+// proj/include/fusedce/fused_backward.hpp:118-140; per-(n, v) work in
+// accumulate_grads_block 26-56) is three contractions over different index
+// pairs: S = H.W^T (recompute, contract d), dH = G.W (contract v) and
+// dW = G^T.H (contract n).  At D = 4096 neither dH[m,:] nor dW[v,:] fits TMEM,
+// so each contraction stays output-stationary on the tensor cores and only
+// G = gamma (softmax - onehot), bf16, moves between them through a 2-slot ring
+// of (row chunk x vocab band) chunks sized to stay L2-resident.
+//
+// Work units of one launch, dispatched in this order by an atomic counter
+// (work stealing, 1 CTA per SM):
+//     G(0) M(0) G(1) M(1) ... G(C-1) M(C-1)
+//   G(c): 128x256 S tiles of chunk c -> G tile into ring slot c % 2
+//   M(c): dH units (128 rows x 256 d, K = band) then dW units (128 vocab rows
+//         x 256 d, K = row chunk) reading ring slot c % 2
+// Dependencies (waited by the TMA producer before it loads a unit, released by
+// the epilogue with a gpu-scope fence + atomic; every wait targets a unit
+// dispatched earlier, so the schedule cannot deadlock):
+//   G(c)        needs M(c-2) complete            (ring slot reuse)
+//   dH(c, mb)   needs G(c) rows of mb complete   and dH(c-1) complete when c
+//               is not the first band of its row chunk (fixed fp32 add order)
+//   dW(c)       needs G(c) complete              and dW(c - bands) complete when
+//               c is not in the first row chunk (store, then ordered adds)
+#include <cmath>
+#include <cstdio>
+
+#include "fce_internal.h"
+#include "sm100_ptx.cuh"
+
+namespace fce {
+
+using namespace ptx;
+
+static constexpr float kL2e = 1.4426950408889634f;
+constexpr int kUnitRing = 4;
+
+enum UnitType : int { kUnitGrad = 0, kUnitDH = 1, kUnitDW = 2, kUnitStop = 3 };
+
+struct BUnit {
+    int type, c, m_blk, n_tile;  // m_blk: rows (grad, dH) or vocab rows (dW); n_tile: vocab tile (grad) or d tile
+};
+
+__device__ __forceinline__ BUnit decode_unit(const BwdParams& p, int u) {
+    BUnit r;
+    if (u >= p.units) {
+        r.type = kUnitStop;
+        return r;
+    }
+    // binary search the segment boundaries: seg 2c = G(c), 2c+1 = M(c)
+    int lo = 0, hi = 2 * p.n_chunks;  // bnd[lo] <= u < bnd[hi]
+    while (hi - lo > 1) {
+        const int mid = (lo + hi) >> 1;
+        if (__ldg(&p.bnd[mid]) <= u)
+            lo = mid;
+        else
+            hi = mid;
+    }
+    const int c = lo >> 1;
+    const int l = u - __ldg(&p.bnd[lo]);
+    const BwdChunk ck = p.chunks[c];
+    r.c = c;
+    if ((lo & 1) == 0) {
+        r.type = kUnitGrad;
+        r.m_blk = l / ck.vt;
+        r.n_tile = l - r.m_blk * ck.vt;
+    } else if (l < ck.n_dh) {
+        r.type = kUnitDH;
+        r.m_blk = l / p.d_tiles;
+        r.n_tile = l - r.m_blk * p.d_tiles;
+    } else {
+        const int l2 = l - ck.n_dh;
+        r.type = kUnitDW;
+        r.n_tile = l2 / ck.vm;
+        r.m_blk = l2 - r.n_tile * ck.vm;
+    }
+    return r;
+}
+
+__device__ __forceinline__ unsigned ld_acquire(const unsigned* ptr) {
+    unsigned v;
+    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(ptr) : "memory");
+    return v;
+}
+
+__device__ __forceinline__ void wait_at_least(const unsigned* ptr, unsigned target) {
+    if (ld_acquire(ptr) >= target) return;
+    while (ld_acquire(ptr) < target) __nanosleep(256);
+}
+
+__device__ __forceinline__ void fence_proxy_async_global() {
+    asm volatile("fence.proxy.async.global;" ::: "memory");
+}
+
+__device__ __forceinline__ void named_bar_sync(int id, int count) {
+    asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(count) : "memory");
+}
+
+__global__ void __launch_bounds__(kThreads, 1)
+    fce_bwd_persistent_kernel(const __grid_constant__ BwdParams p, const __grid_constant__ BwdMaps maps) {
+    extern __shared__ uint8_t smem_raw[];
+    const uint32_t raw_addr = smem_u32(smem_raw);
+    uint8_t* smem = smem_raw + (((raw_addr + 1023u) & ~1023u) - raw_addr);
+    uint8_t* sA = smem;
+    uint8_t* sB = smem + kStages * kStageBytesA;
+    uint64_t* bars = reinterpret_cast<uint64_t*>(sB + kStages * kStageBytesB);
+    uint64_t* full = bars;
+    uint64_t* empty = bars + kStages;
+    uint64_t* tfull = bars + 2 * kStages;
+    uint64_t* tempty = tfull + 2;
+    uint64_t* ufull = tempty + 2;
+    uint64_t* uempty = ufull + kUnitRing;
+    int* unit_ring = reinterpret_cast<int*>(uempty + kUnitRing);
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(unit_ring + kUnitRing);
+
+    const int warp = threadIdx.x >> 5;
+    const int lane = threadIdx.x & 31;
+    unsigned* const ctr = p.counters;
+
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < kStages; ++s) {
+            mbar_init(&full[s], 1);
+            mbar_init(&empty[s], 1);
+        }
+        for (int b = 0; b < 2; ++b) {
+            mbar_init(&tfull[b], 1);
+            mbar_init(&tempty[b], 4);
+        }
+        for (int s = 0; s < kUnitRing; ++s) {
+            mbar_init(&ufull[s], 1);
+            mbar_init(&uempty[s], 5);  // MMA thread + one lane of each epilogue warp
+        }
+        fence_mbar_init();
+    }
+    if (warp == 0 && lane == 0) {
+        tma_prefetch_desc(&maps.h_k);
+        tma_prefetch_desc(&maps.w_k);
+        tma_prefetch_desc(&maps.g_k);
+        tma_prefetch_desc(&maps.w_mn);
+        tma_prefetch_desc(&maps.g_mn);
+        tma_prefetch_desc(&maps.h_mn);
+    }
+    if (warp == 2) tmem_alloc<512>(tmem_slot);
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem_base = *tmem_slot;
+
+    if (warp == 0) {
+        // ------------------------------------------------ scheduler + TMA producer
+        if (lane == 0) {
+            int stage = 0, us = 0;
+            uint32_t phase = 0, uphase = 0;
+            for (;;) {
+                const int u = static_cast<int>(atomicAdd(&ctr[0], 1u));
+                const BUnit un = decode_unit(p, u);
+                mbar_wait(&uempty[us], uphase ^ 1);
+                unit_ring[us] = u;
+                mbar_arrive(&ufull[us]);
+                if (++us == kUnitRing) {
+                    us = 0;
+                    uphase ^= 1;
+                }
+                if (un.type == kUnitStop) break;
+                const BwdChunk ck = p.chunks[un.c];
+                const unsigned* cc = ctr + 1 + 4 * un.c;
+                int kbs;
+                const CUtensorMap *ma, *mb;
+                int a_mn, b_mn, a_row, b_row;  // K-major: row coordinate; MN-major: M/N start
+                int a_k0, b_k0;                // K coordinate base
+                if (un.type == kUnitGrad) {
+                    if (un.c >= 2) {
+                        const BwdChunk& pk = p.chunks[un.c - 2];
+                        wait_at_least(ctr + 1 + 4 * (un.c - 2) + 3, pk.n_dh + pk.n_dw);
+                    }
+                    kbs = p.k_blocks_d;
+                    ma = &maps.h_k;
+                    mb = &maps.w_k;
+                    a_mn = 0;
+                    b_mn = 0;
+                    a_row = ck.r0 + un.m_blk * kBM;
+                    b_row = ck.vb + un.n_tile * kBN;
+                    a_k0 = b_k0 = 0;
+                } else if (un.type == kUnitDH) {
+                    wait_at_least(p.counters + p.gm_base + un.c * p.mb_max + un.m_blk, ck.vt);
+                    if (ck.band_idx > 0) wait_at_least(ctr + 1 + 4 * (un.c - 1) + 1, p.chunks[un.c - 1].n_dh);
+                    kbs = (ck.vc + kBK - 1) / kBK;
+                    ma = &maps.g_k;
+                    mb = &maps.w_mn;
+                    a_mn = 0;
+                    b_mn = 1;
+                    a_row = ck.slot * p.nc_max + un.m_blk * kBM;
+                    b_row = un.n_tile * kBN;
+                    a_k0 = 0;
+                    b_k0 = ck.vb;
+                } else {
+                    wait_at_least(cc + 0, ck.n_g);
+                    if (ck.row_idx > 0) wait_at_least(ctr + 1 + 4 * (un.c - p.bands) + 2, p.chunks[un.c - p.bands].n_dw);
+                    kbs = (ck.nc + kBK - 1) / kBK;
+                    ma = &maps.g_mn;
+                    mb = &maps.h_mn;
+                    a_mn = 1;
+                    b_mn = 1;
+                    a_row = un.m_blk * kBM;
+                    b_row = un.n_tile * kBN;
+                    a_k0 = ck.slot * p.nc_max;
+                    b_k0 = ck.r0;
+                }
+                // order the acquire above before this thread's async-proxy (TMA) reads
+                fence_proxy_async_global();
+                for (int kb = 0; kb < kbs; ++kb) {
+                    mbar_wait(&empty[stage], phase ^ 1);
+                    mbar_arrive_expect_tx(&full[stage], kStageBytesA + kStageBytesB);
+                    uint8_t* a_dst = sA + stage * kStageBytesA;
+                    uint8_t* b_dst = sB + stage * kStageBytesB;
+                    if (!a_mn) {
+                        tma_load_2d(a_dst, ma, &full[stage], a_k0 + kb * kBK, a_row, kEvictNormal);
+                    } else {
+#pragma unroll
+                        for (int j = 0; j < kBM / 64; ++j)
+                            tma_load_2d(a_dst + j * 8192, ma, &full[stage], a_row + 64 * j,
+                                        a_k0 + kb * kBK, kEvictNormal);
+                    }
+                    if (!b_mn) {
+                        tma_load_2d(b_dst, mb, &full[stage], b_k0 + kb * kBK, b_row, kEvictNormal);
+                    } else {
+#pragma unroll
+                        for (int j = 0; j < kBN / 64; ++j)
+                            tma_load_2d(b_dst + j * 8192, mb, &full[stage], b_row + 64 * j,
+                                        b_k0 + kb * kBK, kEvictNormal);
+                    }
+                    if (++stage == kStages) {
+                        stage = 0;
+                        phase ^= 1;
+                    }
+                }
+            }
+        }
+    } else if (warp == 1) {
+        // ------------------------------------------------ MMA issuer
+        if (lane == 0) {
+            int stage = 0, us = 0, acc = 0;
+            uint32_t phase = 0, uphase = 0, acc_phase = 0;
+            for (;;) {
+                mbar_wait(&ufull[us], uphase);
+                const int u = unit_ring[us];
+                mbar_arrive(&uempty[us]);
+                if (++us == kUnitRing) {
+                    us = 0;
+                    uphase ^= 1;
+                }
+                const BUnit un = decode_unit(p, u);
+                if (un.type == kUnitStop) break;
+                const BwdChunk ck = p.chunks[un.c];
+                int kbs, a_mn, b_mn;
+                if (un.type == kUnitGrad) {
+                    kbs = p.k_blocks_d;
+                    a_mn = 0;
+                    b_mn = 0;
+                } else if (un.type == kUnitDH) {
+                    kbs = (ck.vc + kBK - 1) / kBK;
+                    a_mn = 0;
+                    b_mn = 1;
+                } else {
+                    kbs = (ck.nc + kBK - 1) / kBK;
+                    a_mn = 1;
+                    b_mn = 1;
+                }
+                const uint32_t idesc = make_idesc_bf16(kBM, kBN, a_mn, b_mn);
+                mbar_wait(&tempty[acc], acc_phase ^ 1);
+                tc_fence_after();
+                const uint32_t d_tmem = tmem_base + acc * kBN;
+                for (int kb = 0; kb < kbs; ++kb) {
+                    mbar_wait(&full[stage], phase);
+                    tc_fence_after();
+                    const uint32_t a_base = smem_u32(sA + stage * kStageBytesA);
+                    const uint32_t b_base = smem_u32(sB + stage * kStageBytesB);
+#pragma unroll
+                    for (int k = 0; k < kBK / 16; ++k) {
+                        const uint64_t ad = a_mn ? make_sdesc_sw128(a_base + k * 2048, 8192, 1024)
+                                                 : make_sdesc_sw128(a_base + k * 32, 16, 1024);
+                        const uint64_t bd = b_mn ? make_sdesc_sw128(b_base + k * 2048, 8192, 1024)
+                                                 : make_sdesc_sw128(b_base + k * 32, 16, 1024);
+                        umma_bf16(d_tmem, ad, bd, idesc, (kb | k) != 0 ? 1u : 0u);
+                    }
+                    umma_commit(&empty[stage]);
+                    if (++stage == kStages) {
+                        stage = 0;
+                        phase ^= 1;
+                    }
+                }
+                umma_commit(&tfull[acc]);
+                acc ^= 1;
+                if (acc == 0) acc_phase ^= 1;
+            }
+        }
+    } else if (warp >= 4) {
+        // ------------------------------------------------ epilogue
+        const int q = warp & 3;
+        const int r = q * 32 + lane;
+        int us = 0, acc = 0;
+        uint32_t uphase = 0, acc_phase = 0;
+        for (;;) {
+            mbar_wait(&ufull[us], uphase);
+            const int u = unit_ring[us];
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&uempty[us]);
+            if (++us == kUnitRing) {
+                us = 0;
+                uphase ^= 1;
+            }
+            const BUnit un = decode_unit(p, u);
+            if (un.type == kUnitStop) break;
+            const BwdChunk ck = p.chunks[un.c];
+
+            mbar_wait(&tfull[acc], acc_phase);
+            tc_fence_after();
+            const uint32_t taddr = tmem_base + (static_cast<uint32_t>(q * 32) << 16) +
+                                   static_cast<uint32_t>(acc * kBN);
+            if (un.type == kUnitGrad) {
+                const int lrow = un.m_blk * kBM + r;  // row inside the chunk
+                const bool row_ok = lrow < ck.nc;
+                const int64_t grow = static_cast<int64_t>(ck.r0) + lrow;
+                float gam = 0.f, l2lse = 0.f;
+                int64_t tcol = -1;
+                if (row_ok) {
+                    const int64_t y = p.targets[grow];
+                    const bool skip = p.has_ignore && y == p.ignore_index;
+                    gam = skip ? 0.f : p.gamma[grow];
+                    l2lse = skip ? 0.f : p.lse[grow] * kL2e;
+                    tcol = y - (p.v_offset + ck.vb);
+                }
+                __nv_bfloat16* grow_ptr =
+                    p.g_ring + (static_cast<int64_t>(ck.slot) * p.nc_max + lrow) * p.ldg;
+#pragma unroll 1
+                for (int c = 0; c < kBN / 32; ++c) {
+                    float v[32];
+                    tmem_ld32(taddr + c * 32, v);
+                    const int col0 = un.n_tile * kBN + c * 32;
+                    if (row_ok) {
+                        const int64_t tc = tcol - col0;
+                        uint32_t packed[16];
+#pragma unroll
+                        for (int j = 0; j < 32; j += 2) {
+                            float g0 = gam * (ex2(fmaf(v[j], kL2e, -l2lse)) - (tc == j ? 1.f : 0.f));
+                            float g1 = gam * (ex2(fmaf(v[j + 1], kL2e, -l2lse)) - (tc == j + 1 ? 1.f : 0.f));
+                            if (gam == 0.f || col0 + j >= ck.vc) g0 = 0.f;
+                            if (gam == 0.f || col0 + j + 1 >= ck.vc) g1 = 0.f;
+                            packed[j >> 1] = pack_bf16(g0, g1);
+                        }
+                        __nv_bfloat16* dst = grow_ptr + col0;
+#pragma unroll
+                        for (int j = 0; j < 4; ++j)
+                            st_v4_b32(dst + 8 * j, packed[4 * j], packed[4 * j + 1], packed[4 * j + 2],
+                                      packed[4 * j + 3]);
+                    }
+                }
+            } else {
+                // dH: rows = chunk rows, C = dH + (r0 + row) * lddh; dW: rows = band vocab rows
+                const bool is_dh = un.type == kUnitDH;
+                const int lrow = un.m_blk * kBM + r;
+                const int mrows = is_dh ? ck.nc : ck.vc;
+                const bool accumulate = is_dh ? (ck.band_idx > 0 || p.accumulate_dh) : (ck.row_idx > 0);
+                float* crow = is_dh ? p.dh + (static_cast<int64_t>(ck.r0) + lrow) * p.lddh
+                                    : p.dw + (static_cast<int64_t>(ck.vb) + lrow) * p.lddw;
+#pragma unroll 1
+                for (int c = 0; c < kBN / 32; ++c) {
+                    float v[32];
+                    tmem_ld32(taddr + c * 32, v);
+                    const int col0 = un.n_tile * kBN + c * 32;
+                    if (lrow < mrows) {
+                        float* dst = crow + col0;
+                        const bool vec = (col0 + 32 <= p.d) && ((reinterpret_cast<uintptr_t>(dst) & 15) == 0);
+                        if (vec) {
+                            if (accumulate) {
+#pragma unroll
+                                for (int j = 0; j < 32; j += 4) red_add_v4(dst + j, v[j], v[j + 1], v[j + 2], v[j + 3]);
+                            } else {
+#pragma unroll
+                                for (int j = 0; j < 32; j += 4) st_v4(dst + j, v[j], v[j + 1], v[j + 2], v[j + 3]);
+                            }
+                        } else {
+                            for (int j = 0; j < 32; ++j) {
+                                if (col0 + j < p.d) {
+                                    if (accumulate)
+                                        atomicAdd(dst + j, v[j]);
+                                    else
+                                        dst[j] = v[j];
+                                }
+                            }
+                        }
+                    }
+                }
+            }
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&tempty[acc]);
+            acc ^= 1;
+            if (acc == 0) acc_phase ^= 1;
+
+            // publish completion of this unit: all 128 epilogue threads' stores,
+            // then one gpu-scope release
+            fence_proxy_async_global();
+            named_bar_sync(1, 128);
+            if (threadIdx.x == 128) {
+                __threadfence();
+                unsigned* cc = ctr + 1 + 4 * un.c;
+                if (un.type == kUnitGrad) {
+                    atomicAdd(ctr + p.gm_base + un.c * p.mb_max + un.m_blk, 1u);
+                    atomicAdd(cc + 0, 1u);
+                } else if (un.type == kUnitDH) {
+                    atomicAdd(cc + 1, 1u);
+                    atomicAdd(cc + 3, 1u);
+                } else {
+                    atomicAdd(cc + 2, 1u);
+                    atomicAdd(cc + 3, 1u);
+                }
+            }
+        }
+    }
+
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    if (warp == 2) tmem_dealloc<512>(tmem_base);
+}
+
+cudaError_t launch_bwd_persistent(const BwdParams& p, const BwdMaps& maps, int grid,
+                                  cudaStream_t stream) {
+    static bool attr_done = false;
+    const int smem = kSmemBytes + 256;
+    if (!attr_done) {
+        cudaError_t e = cudaFuncSetAttribute(fce_bwd_persistent_kernel,
+                                             cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        if (e != cudaSuccess) return e;
+        attr_done = true;
+    }
+    if (grid > p.units) grid = p.units;
+    if (grid < 1) return cudaSuccess;
+    fce_bwd_persistent_kernel<<<grid, kThreads, smem, stream>>>(p, maps);
+    return cudaGetLastError();
+}
+
+}  // namespace fce

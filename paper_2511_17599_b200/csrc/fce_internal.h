@@ -66,6 +66,39 @@ struct TensorMaps {
     CUtensorMap a0, b0, a1, b1;
 };
 
+// ----------------------------------------------------------- persistent backward
+// One (row chunk x vocab band) chunk of the backward (fce_bwd.cu).
+struct BwdChunk {
+    int r0, nc;          // rows [r0, r0 + nc)
+    int vb, vc;          // local vocab rows [vb, vb + vc)
+    int slot;            // G ring slot
+    int row_idx, band_idx;
+    int vt, vm;          // vocab tiles of 256 (grad units per m-block) / of 128 (dW rows)
+    int n_g, n_dh, n_dw; // unit counts
+};
+
+struct BwdParams {
+    int units, n_chunks, bands, d_tiles, k_blocks_d, mb_max, gm_base;
+    int has_ignore, accumulate_dh;
+    int64_t nc_max, ldg, d, lddh, lddw, v_offset, ignore_index;
+    const BwdChunk* chunks;
+    const int* bnd;          // 2 * n_chunks + 1 segment boundaries
+    unsigned* counters;      // [0] scheduler, 4 per chunk, then mb_max per chunk
+    const int64_t* targets;
+    const float* lse;
+    const float* gamma;
+    __nv_bfloat16* g_ring;   // [2][nc_max][ldg]
+    float* dh;
+    float* dw;
+};
+
+struct BwdMaps {
+    CUtensorMap h_k, w_k, g_k, w_mn, g_mn, h_mn;
+};
+
+cudaError_t launch_bwd_persistent(const BwdParams& p, const BwdMaps& maps, int grid,
+                                  cudaStream_t stream);
+
 // Stream a handle launches on (fce_api.cpp).
 cudaStream_t handle_stream(fce_handle h);
 // Thread-local message returned by fce_last_error (fce_api.cpp).
