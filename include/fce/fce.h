@@ -142,6 +142,14 @@ fce_status fce_backward(fce_handle h, const fce_problem* p, fce_stats stats, int
                         float upstream_scalar, const float* upstream_rows, float* dhidden,
                         int64_t lddh, float* dweight, int64_t lddw, int accumulate_dhidden);
 
+/* The tile kernel's generic contraction (the dW / dH building block), exposed
+ * for kernel-level tests and benchmarks: C[M, N] (+)= A . B^T in fp32 with bf16
+ * operands; A is [M, K] (a_mn = 0, row stride lda) or stored as [K, M]
+ * (a_mn = 1); B is [N, K] (b_mn = 0) or stored as [K, N] (b_mn = 1). */
+fce_status fce_gemm_bf16(fce_handle h, const void* a, int64_t lda, int a_mn, const void* b,
+                         int64_t ldb, int b_mn, int64_t m, int64_t n, int64_t k, float* c,
+                         int64_t ldc, int accumulate);
+
 /* scale_partial_grads (fused_backward.hpp:193-202): x[i] *= factor. */
 fce_status fce_scale(fce_handle h, float* x, int64_t count, float factor);
 

@@ -79,7 +79,7 @@ class FceStats(ctypes.Structure):
 EXPORTED_SYMBOLS = [
     "fce_create", "fce_destroy", "fce_set_stream", "fce_last_error", "fce_status_string",
     "fce_set_option", "fce_workspace_bytes", "fce_launch_count", "fce_kernel_stats", "fce_forward",
-    "fce_forward_partial", "fce_merge_partials", "fce_backward", "fce_scale",
+    "fce_forward_partial", "fce_merge_partials", "fce_backward", "fce_gemm_bf16", "fce_scale",
     "fce_generate_instance", "fce_f32_to_bf16",
     "fce_comm_unique_id", "fce_comm_init", "fce_comm_destroy", "fce_vp_last_error",
     "fce_vp_forward", "fce_vp_backward",
@@ -114,6 +114,7 @@ def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
         "fce_merge_partials": (I32, [P, I32, I64, I64, P, P, P, P, P, I32, I64, I32, FceStats, P, P, P]),
         "fce_backward": (I32, [P, ctypes.POINTER(FceProblem), FceStats, I32, F, P, P, I64, P, I64, I32]),
         "fce_scale": (I32, [P, P, I64, F]),
+        "fce_gemm_bf16": (I32, [P, P, I64, I32, P, I64, I32, I64, I64, I64, P, I64, I32]),
         "fce_generate_instance": (I32, [P, I64, I64, I64, ctypes.c_uint64, P, I64, P, I64, P, I64, D, P, P]),
         "fce_f32_to_bf16": (I32, [P, P, I64, I64, I64, P, I64]),
         "fce_comm_unique_id": (I32, [P, ctypes.c_size_t]),
@@ -359,6 +360,27 @@ def fused_forward_with_partial_grads(hidden, weight, targets, reduction="mean", 
     dh, dw = fused_backward_recompute(hidden, weight, targets, out.stats, "sum", 1.0,
                                       ignore_index, handle)
     return out, (dh, dw)
+
+
+def gemm_bf16(a, b, a_mn: bool = False, b_mn: bool = False, out=None, accumulate=False,
+              handle=None):
+    """C = A . B^T (fp32) on the tile kernel; A is [M, K] or, with a_mn, [K, M];
+    B is [N, K] or, with b_mn, [K, N].  Test / benchmark entry of the contraction."""
+    import torch
+    h = handle or default_handle(a.device.index or 0)
+    a = _as_operand(a, "a")
+    b = _as_operand(b, "b")
+    m = a.shape[1] if a_mn else a.shape[0]
+    k = a.shape[0] if a_mn else a.shape[1]
+    n = b.shape[1] if b_mn else b.shape[0]
+    kb = b.shape[0] if b_mn else b.shape[1]
+    if k != kb:
+        raise DimensionMismatch(f"K mismatch {k} != {kb}")
+    if out is None:
+        out = torch.zeros(m, n, dtype=torch.float32, device=a.device)
+    _check(h.lib.fce_gemm_bf16(h.raw, a.data_ptr(), a.stride(0), int(a_mn), b.data_ptr(), b.stride(0),
+                               int(b_mn), m, n, k, out.data_ptr(), out.stride(0), int(accumulate)))
+    return out
 
 
 def scale_partial_grads(partials, gamma_eff: float, handle=None):

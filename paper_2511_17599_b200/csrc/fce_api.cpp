@@ -758,6 +758,47 @@ fce_status fce_backward(fce_handle h, const fce_problem* p, fce_stats stats, int
     return FCE_OK;
 }
 
+fce_status fce_gemm_bf16(fce_handle h, const void* a, int64_t lda, int a_mn, const void* b,
+                         int64_t ldb, int b_mn, int64_t m, int64_t n, int64_t k, float* c,
+                         int64_t ldc, int accumulate) {
+    fce_status s = check_handle(h);
+    if (s) return s;
+    if (m <= 0 || n <= 0 || k <= 0) return fail(FCE_EMPTY_INPUT, "gemm requires M, N, K > 0");
+    if (!a || !b || !c) return fail(FCE_INVALID_ARGUMENT, "null operand");
+    if (lda % 8 || ldb % 8 || !aligned16(a) || !aligned16(b))
+        return fail(FCE_INVALID_LAYOUT, "bf16 operands need ld %% 8 == 0 and 16-byte aligned bases");
+    if (m > INT32_MAX / 2 || n > INT32_MAX / 2 || k > INT32_MAX / 2)
+        return fail(FCE_INVALID_LAYOUT, "gemm too large");
+    TileParams gp;
+    std::memset(&gp, 0, sizeof(gp));
+    TensorMaps gm;
+    std::memset(&gm, 0, sizeof(gm));
+    // A: [M, K] K-major (lda >= K) or stored [K, M] MN-major (lda >= M)
+    const bool ok_a = a_mn ? encode_map_2d(&gm.a0, a, m, k, lda * 2, 64, 64)
+                           : encode_map_2d(&gm.a0, a, k, m, lda * 2, kBK, kBM);
+    const bool ok_b = b_mn ? encode_map_2d(&gm.b0, b, n, k, ldb * 2, 64, 64)
+                           : encode_map_2d(&gm.b0, b, k, n, ldb * 2, kBK, kBN);
+    if (!ok_a || !ok_b) return fail(FCE_CUDA_ERROR, "cuTensorMapEncodeTiled failed (gemm)");
+    GemmProblem& q = gp.prob[0];
+    q.m = static_cast<int>(m);
+    q.n = static_cast<int>(n);
+    q.k_blocks = static_cast<int>(ceil_div(k, kBK));
+    q.m_tiles = static_cast<int>(ceil_div(m, kBM));
+    q.n_tiles = static_cast<int>(ceil_div(n, kBN));
+    q.a_mn = a_mn ? 1 : 0;
+    q.b_mn = b_mn ? 1 : 0;
+    q.n_fastest = 0;
+    q.accumulate = accumulate ? 1 : 0;
+    q.c = c;
+    q.ldc = ldc;
+    gp.mode = kEpiGemm;
+    gp.units0 = q.m_tiles * q.n_tiles;
+    gp.units = gp.units0;
+    cudaError_t e = timed_launch(h, gp, gm, 2.0 * m * n * k);
+    if (e != cudaSuccess) return fail(FCE_CUDA_ERROR, "gemm tile kernel: %s", cudaGetErrorString(e));
+    return FCE_OK;
+}
+
 fce_status fce_scale(fce_handle h, float* x, int64_t count, float factor) {
     fce_status s = check_handle(h);
     if (s) return s;
