@@ -53,6 +53,7 @@ struct fce_handle_s {
     unsigned long long* count = nullptr;    // valid-target count
     int* host_err = nullptr;                // pinned mirror
     int64_t splits = 0, band_cols = 0, row_chunk = 0, validate = 1, bwd_persistent = 1;
+    int64_t l2_hints = 1;
     int64_t launches = 0;
     size_t bwd_scratch[4] = {0, 0, 0, 0};  // offsets of the persistent-backward scratch
     // optional per-kernel CUDA-event timing of the tile kernels (bench roofline)
@@ -334,6 +335,7 @@ fce_status run_backward_persistent(fce_handle h, const fce_problem* p, const flo
     bp.gm_base = static_cast<int>(1 + 4 * n_chunks);
     bp.has_ignore = p->has_ignore;
     bp.accumulate_dh = accumulate_dhidden;
+    bp.l2_hints = static_cast<int>(h->l2_hints);
     bp.nc_max = row_chunk;
     bp.ldg = band;
     bp.d = p->d;
@@ -462,6 +464,8 @@ fce_status fce_set_option(fce_handle h, const char* key, int64_t value) {
         h->row_chunk = value;
     } else if (!std::strcmp(key, "validate")) {
         h->validate = value ? 1 : 0;
+    } else if (!std::strcmp(key, "l2_hints")) {
+        h->l2_hints = value;
     } else if (!std::strcmp(key, "bwd_persistent")) {
         h->bwd_persistent = value ? 1 : 0;
     } else if (!std::strcmp(key, "timing")) {
@@ -788,7 +792,7 @@ fce_status fce_gemm_bf16(fce_handle h, const void* a, int64_t lda, int a_mn, con
     q.a_mn = a_mn ? 1 : 0;
     q.b_mn = b_mn ? 1 : 0;
     q.n_fastest = 0;
-    q.accumulate = accumulate ? 1 : 0;
+    q.accumulate = accumulate == 2 ? 2 : (accumulate ? 1 : 0);
     q.c = c;
     q.ldc = ldc;
     gp.mode = kEpiGemm;

@@ -152,6 +152,9 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (lane == 0) {
             int stage = 0, us = 0;
             uint32_t phase = 0, uphase = 0;
+            const uint64_t pol_norm = policy_evict_normal();
+            const uint64_t pol_g = (p.l2_hints & 2) ? policy_evict_last() : pol_norm;
+            const uint64_t pol_h = (p.l2_hints & 8) ? policy_evict_first() : pol_norm;
             for (;;) {
                 const int u = static_cast<int>(atomicAdd(&ctr[0], 1u));
                 const BUnit un = decode_unit(p, u);
@@ -169,6 +172,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                 const CUtensorMap *ma, *mb;
                 int a_mn, b_mn, a_row, b_row;  // K-major: row coordinate; MN-major: M/N start
                 int a_k0, b_k0;                // K coordinate base
+                uint64_t pa = pol_norm, pb = pol_norm;
                 if (un.type == kUnitGrad) {
                     if (un.c >= 2) {
                         const BwdChunk& pk = p.chunks[un.c - 2];
@@ -194,6 +198,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                     b_row = un.n_tile * kBN;
                     a_k0 = 0;
                     b_k0 = ck.vb;
+                    pa = pol_g;
                 } else {
                     wait_at_least(cc + 0, ck.n_g);
                     if (ck.row_idx > 0) wait_at_least(ctr + 1 + 4 * (un.c - p.bands) + 2, p.chunks[un.c - p.bands].n_dw);
@@ -206,6 +211,8 @@ __global__ void __launch_bounds__(kThreads, 1)
                     b_row = un.n_tile * kBN;
                     a_k0 = ck.slot * p.nc_max;
                     b_k0 = ck.r0;
+                    pa = pol_g;
+                    pb = pol_h;
                 }
                 // order the acquire above before this thread's async-proxy (TMA) reads
                 fence_proxy_async_global();
@@ -215,20 +222,20 @@ __global__ void __launch_bounds__(kThreads, 1)
                     uint8_t* a_dst = sA + stage * kStageBytesA;
                     uint8_t* b_dst = sB + stage * kStageBytesB;
                     if (!a_mn) {
-                        tma_load_2d(a_dst, ma, &full[stage], a_k0 + kb * kBK, a_row, kEvictNormal);
+                        tma_load_2d(a_dst, ma, &full[stage], a_k0 + kb * kBK, a_row, pa);
                     } else {
 #pragma unroll
                         for (int j = 0; j < kBM / 64; ++j)
                             tma_load_2d(a_dst + j * 8192, ma, &full[stage], a_row + 64 * j,
-                                        a_k0 + kb * kBK, kEvictNormal);
+                                        a_k0 + kb * kBK, pa);
                     }
                     if (!b_mn) {
-                        tma_load_2d(b_dst, mb, &full[stage], b_k0 + kb * kBK, b_row, kEvictNormal);
+                        tma_load_2d(b_dst, mb, &full[stage], b_k0 + kb * kBK, b_row, pb);
                     } else {
 #pragma unroll
                         for (int j = 0; j < kBN / 64; ++j)
                             tma_load_2d(b_dst + j * 8192, mb, &full[stage], b_row + 64 * j,
-                                        b_k0 + kb * kBK, kEvictNormal);
+                                        b_k0 + kb * kBK, pb);
                     }
                     if (++stage == kStages) {
                         stage = 0;
@@ -301,6 +308,8 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int r = q * 32 + lane;
         int us = 0, acc = 0;
         uint32_t uphase = 0, acc_phase = 0;
+        const uint64_t pol_out = (p.l2_hints & 1) ? policy_evict_first() : policy_evict_normal();
+        const uint64_t pol_gst = (p.l2_hints & 4) ? policy_evict_last() : policy_evict_normal();
         for (;;) {
             mbar_wait(&ufull[us], uphase);
             const int u = unit_ring[us];
@@ -352,8 +361,8 @@ __global__ void __launch_bounds__(kThreads, 1)
                         __nv_bfloat16* dst = grow_ptr + col0;
 #pragma unroll
                         for (int j = 0; j < 4; ++j)
-                            st_v4_b32(dst + 8 * j, packed[4 * j], packed[4 * j + 1], packed[4 * j + 2],
-                                      packed[4 * j + 3]);
+                            st_v4_b32_hint(dst + 8 * j, packed[4 * j], packed[4 * j + 1], packed[4 * j + 2],
+                                           packed[4 * j + 3], pol_gst);
                     }
                 }
             } else {
@@ -375,10 +384,12 @@ __global__ void __launch_bounds__(kThreads, 1)
                         if (vec) {
                             if (accumulate) {
 #pragma unroll
-                                for (int j = 0; j < 32; j += 4) red_add_v4(dst + j, v[j], v[j + 1], v[j + 2], v[j + 3]);
+                                for (int j = 0; j < 32; j += 4)
+                                    red_add_v4_hint(dst + j, v[j], v[j + 1], v[j + 2], v[j + 3], pol_out);
                             } else {
 #pragma unroll
-                                for (int j = 0; j < 32; j += 4) st_v4(dst + j, v[j], v[j + 1], v[j + 2], v[j + 3]);
+                                for (int j = 0; j < 32; j += 4)
+                                    st_v4_hint(dst + j, v[j], v[j + 1], v[j + 2], v[j + 3], pol_out);
                             }
                         } else {
                             for (int j = 0; j < 32; ++j) {

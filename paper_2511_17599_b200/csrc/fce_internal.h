@@ -80,6 +80,8 @@ struct BwdChunk {
 struct BwdParams {
     int units, n_chunks, bands, d_tiles, k_blocks_d, mb_max, gm_base;
     int has_ignore, accumulate_dh;
+    int l2_hints;            // bit0: evict_first on dH/dW writes, bit1: evict_last on G loads,
+                             // bit2: evict_last on G stores, bit3: evict_first on H loads (dW)
     int64_t nc_max, ldg, d, lddh, lddw, v_offset, ignore_index;
     const BwdChunk* chunks;
     const int* bnd;          // 2 * n_chunks + 1 segment boundaries

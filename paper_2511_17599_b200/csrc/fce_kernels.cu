@@ -312,7 +312,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                         }
                     } else {
                         const GemmProblem& gq = p.prob[un.prob];
-                        if (row < gq.m) {
+                        if (row < gq.m && gq.accumulate != 2) {  // 2: discard (benchmark only)
                             float* dst = gq.c + row * gq.ldc + col0;
                             const bool vec = (col0 + 32 <= gq.n) &&
                                              ((reinterpret_cast<uintptr_t>(dst) & 15) == 0);

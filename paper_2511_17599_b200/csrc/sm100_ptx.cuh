@@ -173,6 +173,43 @@ __device__ __forceinline__ void red_add_v4(float* addr, float a, float b, float 
                  : "memory");
 }
 
+__device__ __forceinline__ void red_add_v4_hint(float* addr, float a, float b, float c, float d,
+                                                uint64_t pol) {
+    asm volatile("red.global.add.L2::cache_hint.v4.f32 [%0], {%1, %2, %3, %4}, %5;" ::"l"(addr),
+                 "f"(a), "f"(b), "f"(c), "f"(d), "l"(pol)
+                 : "memory");
+}
+
+__device__ __forceinline__ void st_v4_hint(float* addr, float a, float b, float c, float d,
+                                           uint64_t pol) {
+    asm volatile("st.global.L2::cache_hint.v4.f32 [%0], {%1, %2, %3, %4}, %5;" ::"l"(addr), "f"(a),
+                 "f"(b), "f"(c), "f"(d), "l"(pol)
+                 : "memory");
+}
+
+__device__ __forceinline__ void st_v4_b32_hint(void* addr, uint32_t a, uint32_t b, uint32_t c,
+                                               uint32_t d, uint64_t pol) {
+    asm volatile("st.global.L2::cache_hint.v4.b32 [%0], {%1, %2, %3, %4}, %5;" ::"l"(addr), "r"(a),
+                 "r"(b), "r"(c), "r"(d), "l"(pol)
+                 : "memory");
+}
+
+__device__ __forceinline__ uint64_t policy_evict_first() {
+    uint64_t q;
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(q));
+    return q;
+}
+__device__ __forceinline__ uint64_t policy_evict_last() {
+    uint64_t q;
+    asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(q));
+    return q;
+}
+__device__ __forceinline__ uint64_t policy_evict_normal() {
+    uint64_t q;
+    asm volatile("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;" : "=l"(q));
+    return q;
+}
+
 __device__ __forceinline__ void st_v4(float* addr, float a, float b, float c, float d) {
     asm volatile("st.global.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(addr), "f"(a), "f"(b), "f"(c),
                  "f"(d)
