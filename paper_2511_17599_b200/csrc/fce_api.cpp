@@ -272,42 +272,49 @@ fce_status run_backward_persistent(fce_handle h, const fce_problem* p, const flo
                                    int accumulate_dhidden) {
     char* ws = static_cast<char*>(h->ws);
     __nv_bfloat16* g_ring = reinterpret_cast<__nv_bfloat16*>(ws + h->bwd_scratch[0]);
-    BwdChunk* d_tab = reinterpret_cast<BwdChunk*>(ws + h->bwd_scratch[1]);
-    int* d_bnd = reinterpret_cast<int*>(ws + h->bwd_scratch[2]);
     unsigned* d_ctr = reinterpret_cast<unsigned*>(ws + h->bwd_scratch[3]);
 
     const int64_t n_rc = ceil_div(p->n, row_chunk), n_bd = ceil_div(p->v, band);
     const int64_t n_chunks = n_rc * n_bd;
-    const int mb_max = static_cast<int>(ceil_div(row_chunk, kBM));
+    const int mb_max = static_cast<int>(row_chunk / kBM);
     const int d_tiles = static_cast<int>(ceil_div(p->d, kBN));
-    std::vector<BwdChunk> tab(n_chunks);
-    std::vector<int> bnd(2 * n_chunks + 1);
-    int64_t u = 0;
-    for (int64_t c = 0; c < n_chunks; ++c) {
-        BwdChunk& k = tab[c];
-        const int64_t ri = c / n_bd, bi = c % n_bd;
-        k.r0 = static_cast<int>(ri * row_chunk);
-        k.nc = static_cast<int>(std::min(row_chunk, p->n - ri * row_chunk));
-        k.vb = static_cast<int>(bi * band);
-        k.vc = static_cast<int>(std::min(band, p->v - bi * band));
-        k.slot = static_cast<int>(c & 1);
-        k.row_idx = static_cast<int>(ri);
-        k.band_idx = static_cast<int>(bi);
-        k.vt = static_cast<int>(ceil_div(k.vc, kBN));
-        k.vm = static_cast<int>(ceil_div(k.vc, kBM));
-        const int mbs = static_cast<int>(ceil_div(k.nc, kBM));
-        k.n_g = mbs * k.vt;
-        k.n_dh = dhidden ? mbs * d_tiles : 0;
-        k.n_dw = dweight ? k.vm * d_tiles : 0;
-        bnd[2 * c] = static_cast<int>(u);
-        u += k.n_g;
-        bnd[2 * c + 1] = static_cast<int>(u);
-        u += k.n_dh + k.n_dw;
-    }
-    bnd[2 * n_chunks] = static_cast<int>(u);
-    if (u >= INT32_MAX) return fail(FCE_INVALID_LAYOUT, "too many backward work units");
-    FCE_CUDA(cudaMemcpyAsync(d_tab, tab.data(), sizeof(BwdChunk) * n_chunks, cudaMemcpyHostToDevice, h->stream));
-    FCE_CUDA(cudaMemcpyAsync(d_bnd, bnd.data(), sizeof(int) * bnd.size(), cudaMemcpyHostToDevice, h->stream));
+    BwdParams bp;
+    std::memset(&bp, 0, sizeof(bp));
+    bp.n_chunks = static_cast<int>(n_chunks);
+    bp.bands = static_cast<int>(n_bd);
+    bp.vt = static_cast<int>(band / kBN);
+    bp.vm = static_cast<int>(band / kBM);
+    bp.n_g = mb_max * bp.vt;
+    bp.n_dh = dhidden ? mb_max * d_tiles : 0;
+    bp.n_dw = dweight ? bp.vm * d_tiles : 0;
+    bp.per_chunk = bp.n_g + bp.n_dh + bp.n_dw;
+    const int64_t units = n_chunks * bp.per_chunk;
+    if (units >= INT32_MAX) return fail(FCE_INVALID_LAYOUT, "too many backward work units");
+    bp.units = static_cast<int>(units);
+    bp.d_tiles = d_tiles;
+    bp.k_blocks_d = static_cast<int>(ceil_div(p->d, kBK));
+    bp.mb_max = mb_max;
+    bp.gm_base = static_cast<int>(1 + 4 * n_chunks);
+    bp.n = static_cast<int>(p->n);
+    bp.v = static_cast<int>(p->v);
+    bp.has_ignore = p->has_ignore;
+    bp.accumulate_dh = accumulate_dhidden;
+    bp.l2_hints = static_cast<int>(h->l2_hints);
+    bp.nc_max = row_chunk;
+    bp.ldg = band;
+    bp.d = p->d;
+    bp.lddh = lddh;
+    bp.lddw = lddw;
+    bp.v_offset = p->v_offset;
+    bp.ignore_index = p->ignore_index;
+    bp.counters = d_ctr;
+    bp.targets = p->targets;
+    bp.lse = lse;
+    bp.gamma = gamma;
+    bp.g_ring = g_ring;
+    bp.dh = dhidden;
+    bp.dw = dweight;
+
     FCE_CUDA(cudaMemsetAsync(d_ctr, 0, sizeof(unsigned) * (1 + 4 * n_chunks + n_chunks * mb_max), h->stream));
     // stale ring rows past a short last chunk are read (then masked or
     // multiplied by zero-filled operands): keep them finite
@@ -323,35 +330,6 @@ fce_status run_backward_persistent(fce_handle h, const fce_problem* p, const flo
         !encode_map_2d(&maps.g_mn, g_ring, band, ring_rows, band * 2, 64, 64) ||
         !encode_map_2d(&maps.h_mn, p->hidden, p->d, p->n, p->ldh * 2, 64, 64))
         return fail(FCE_CUDA_ERROR, "cuTensorMapEncodeTiled failed (persistent backward)");
-
-    BwdParams bp;
-    std::memset(&bp, 0, sizeof(bp));
-    bp.units = static_cast<int>(u);
-    bp.n_chunks = static_cast<int>(n_chunks);
-    bp.bands = static_cast<int>(n_bd);
-    bp.d_tiles = d_tiles;
-    bp.k_blocks_d = static_cast<int>(ceil_div(p->d, kBK));
-    bp.mb_max = mb_max;
-    bp.gm_base = static_cast<int>(1 + 4 * n_chunks);
-    bp.has_ignore = p->has_ignore;
-    bp.accumulate_dh = accumulate_dhidden;
-    bp.l2_hints = static_cast<int>(h->l2_hints);
-    bp.nc_max = row_chunk;
-    bp.ldg = band;
-    bp.d = p->d;
-    bp.lddh = lddh;
-    bp.lddw = lddw;
-    bp.v_offset = p->v_offset;
-    bp.ignore_index = p->ignore_index;
-    bp.chunks = d_tab;
-    bp.bnd = d_bnd;
-    bp.counters = d_ctr;
-    bp.targets = p->targets;
-    bp.lse = lse;
-    bp.gamma = gamma;
-    bp.g_ring = g_ring;
-    bp.dh = dhidden;
-    bp.dw = dweight;
 
     cudaEvent_t e0 = nullptr, e1 = nullptr;
     if (h->timing) {
@@ -647,8 +625,7 @@ fce_status fce_backward(fce_handle h, const fce_problem* p, fce_stats stats, int
     const int64_t n_rc = ceil_div(p->n, row_chunk), n_bd = ceil_div(p->v, band);
     const int64_t n_chunks = n_rc * n_bd;
     const int64_t mb_max = ceil_div(row_chunk, kBM);
-    const size_t o_tab = sc.take(sizeof(BwdChunk) * n_chunks);
-    const size_t o_bnd = sc.take(sizeof(int) * (2 * n_chunks + 1));
+    const size_t o_tab = 0, o_bnd = 0;
     const size_t o_ctr = sc.take(sizeof(unsigned) * (1 + 4 * n_chunks + n_chunks * mb_max));
     if ((s = sc.commit())) return s;
     h->bwd_scratch[0] = o_G;

@@ -15,6 +15,9 @@
 //   G(c): 128x256 S tiles of chunk c -> G tile into ring slot c % 2
 //   M(c): dH units (128 rows x 256 d, K = band) then dW units (128 vocab rows
 //         x 256 d, K = row chunk) reading ring slot c % 2
+// Every chunk is counted at full (row_chunk x band) geometry so a unit index
+// decodes with two divisions; units that fall past N or V in the last row
+// chunk / band are empty (no loads, no MMA) but still signal completion.
 // Dependencies (waited by the TMA producer before it loads a unit, released by
 // the epilogue with a gpu-scope fence + atomic; every wait targets a unit
 // dispatched earlier, so the schedule cannot deadlock):
@@ -39,41 +42,50 @@ constexpr int kUnitRing = 4;
 enum UnitType : int { kUnitGrad = 0, kUnitDH = 1, kUnitDW = 2, kUnitStop = 3 };
 
 struct BUnit {
-    int type, c, m_blk, n_tile;  // m_blk: rows (grad, dH) or vocab rows (dW); n_tile: vocab tile (grad) or d tile
+    int type;     // UnitType
+    int c;        // chunk
+    int m_blk;    // 128-row block: chunk rows (grad, dH) or band vocab rows (dW)
+    int n_tile;   // 256-wide tile: band vocab (grad) or d (dH, dW)
+    int r0, nc;   // chunk rows [r0, r0 + nc)
+    int vb, vc;   // band vocab rows [vb, vb + vc)
+    int slot, row_idx, band_idx;
+    bool empty;   // past N or V: no loads / MMA / stores, completion only
 };
 
 __device__ __forceinline__ BUnit decode_unit(const BwdParams& p, int u) {
     BUnit r;
     if (u >= p.units) {
         r.type = kUnitStop;
+        r.empty = true;
         return r;
     }
-    // binary search the segment boundaries: seg 2c = G(c), 2c+1 = M(c)
-    int lo = 0, hi = 2 * p.n_chunks;  // bnd[lo] <= u < bnd[hi]
-    while (hi - lo > 1) {
-        const int mid = (lo + hi) >> 1;
-        if (__ldg(&p.bnd[mid]) <= u)
-            lo = mid;
-        else
-            hi = mid;
-    }
-    const int c = lo >> 1;
-    const int l = u - __ldg(&p.bnd[lo]);
-    const BwdChunk ck = p.chunks[c];
+    const int c = u / p.per_chunk;
+    const int l = u - c * p.per_chunk;
     r.c = c;
-    if ((lo & 1) == 0) {
+    r.row_idx = c / p.bands;
+    r.band_idx = c - r.row_idx * p.bands;
+    r.slot = c & 1;
+    r.r0 = r.row_idx * static_cast<int>(p.nc_max);
+    r.nc = min(static_cast<int>(p.nc_max), p.n - r.r0);
+    r.vb = r.band_idx * static_cast<int>(p.ldg);
+    r.vc = min(static_cast<int>(p.ldg), p.v - r.vb);
+    if (l < p.n_g) {
         r.type = kUnitGrad;
-        r.m_blk = l / ck.vt;
-        r.n_tile = l - r.m_blk * ck.vt;
-    } else if (l < ck.n_dh) {
+        r.m_blk = l / p.vt;
+        r.n_tile = l - r.m_blk * p.vt;
+        r.empty = r.m_blk * kBM >= r.nc || r.n_tile * kBN >= r.vc;
+    } else if (l < p.n_g + p.n_dh) {
+        const int l2 = l - p.n_g;
         r.type = kUnitDH;
-        r.m_blk = l / p.d_tiles;
-        r.n_tile = l - r.m_blk * p.d_tiles;
+        r.m_blk = l2 / p.d_tiles;
+        r.n_tile = l2 - r.m_blk * p.d_tiles;
+        r.empty = r.m_blk * kBM >= r.nc;
     } else {
-        const int l2 = l - ck.n_dh;
+        const int l2 = l - p.n_g - p.n_dh;
         r.type = kUnitDW;
-        r.n_tile = l2 / ck.vm;
-        r.m_blk = l2 - r.n_tile * ck.vm;
+        r.n_tile = l2 / p.vm;
+        r.m_blk = l2 - r.n_tile * p.vm;
+        r.empty = r.m_blk * kBM >= r.vc;
     }
     return r;
 }
@@ -86,7 +98,7 @@ __device__ __forceinline__ unsigned ld_acquire(const unsigned* ptr) {
 
 __device__ __forceinline__ void wait_at_least(const unsigned* ptr, unsigned target) {
     if (ld_acquire(ptr) >= target) return;
-    while (ld_acquire(ptr) < target) __nanosleep(256);
+    while (ld_acquire(ptr) < target) __nanosleep(128);
 }
 
 __device__ __forceinline__ void fence_proxy_async_global() {
@@ -95,6 +107,18 @@ __device__ __forceinline__ void fence_proxy_async_global() {
 
 __device__ __forceinline__ void named_bar_sync(int id, int count) {
     asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(count) : "memory");
+}
+
+// counters: [0] scheduler; chunk c: [1+4c] G done, [2+4c] dH done, [3+4c] dW done,
+// [4+4c] M (dH + dW) done; then per (chunk, 128-row block) G done.
+__device__ __forceinline__ unsigned* cnt(const BwdParams& p, int c, int k) {
+    return p.counters + 1 + 4 * c + k;
+}
+
+__device__ __forceinline__ int unit_kblocks(const BwdParams& p, const BUnit& un) {
+    if (un.type == kUnitGrad) return p.k_blocks_d;
+    if (un.type == kUnitDH) return (un.vc + kBK - 1) / kBK;
+    return (un.nc + kBK - 1) / kBK;
 }
 
 __global__ void __launch_bounds__(kThreads, 1)
@@ -116,7 +140,6 @@ __global__ void __launch_bounds__(kThreads, 1)
 
     const int warp = threadIdx.x >> 5;
     const int lane = threadIdx.x & 31;
-    unsigned* const ctr = p.counters;
 
     if (threadIdx.x == 0) {
         for (int s = 0; s < kStages; ++s) {
@@ -155,8 +178,9 @@ __global__ void __launch_bounds__(kThreads, 1)
             const uint64_t pol_norm = policy_evict_normal();
             const uint64_t pol_g = (p.l2_hints & 2) ? policy_evict_last() : pol_norm;
             const uint64_t pol_h = (p.l2_hints & 8) ? policy_evict_first() : pol_norm;
+            int u_next = static_cast<int>(atomicAdd(p.counters, 1u));
             for (;;) {
-                const int u = static_cast<int>(atomicAdd(&ctr[0], 1u));
+                const int u = u_next;
                 const BUnit un = decode_unit(p, u);
                 mbar_wait(&uempty[us], uphase ^ 1);
                 unit_ring[us] = u;
@@ -166,56 +190,49 @@ __global__ void __launch_bounds__(kThreads, 1)
                     uphase ^= 1;
                 }
                 if (un.type == kUnitStop) break;
-                const BwdChunk ck = p.chunks[un.c];
-                const unsigned* cc = ctr + 1 + 4 * un.c;
-                int kbs;
+                // claim the next unit now; the atomic's latency hides behind this
+                // unit's loads (its result is first used at the top of the loop)
+                u_next = static_cast<int>(atomicAdd(p.counters, 1u));
+                if (un.empty) continue;
                 const CUtensorMap *ma, *mb;
-                int a_mn, b_mn, a_row, b_row;  // K-major: row coordinate; MN-major: M/N start
-                int a_k0, b_k0;                // K coordinate base
+                int a_mn, b_mn, a_row, b_row, a_k0, b_k0;
                 uint64_t pa = pol_norm, pb = pol_norm;
                 if (un.type == kUnitGrad) {
-                    if (un.c >= 2) {
-                        const BwdChunk& pk = p.chunks[un.c - 2];
-                        wait_at_least(ctr + 1 + 4 * (un.c - 2) + 3, pk.n_dh + pk.n_dw);
-                    }
-                    kbs = p.k_blocks_d;
+                    if (un.c >= 2) wait_at_least(cnt(p, un.c - 2, 3), p.n_dh + p.n_dw);
                     ma = &maps.h_k;
                     mb = &maps.w_k;
-                    a_mn = 0;
-                    b_mn = 0;
-                    a_row = ck.r0 + un.m_blk * kBM;
-                    b_row = ck.vb + un.n_tile * kBN;
+                    a_mn = b_mn = 0;
+                    a_row = un.r0 + un.m_blk * kBM;
+                    b_row = un.vb + un.n_tile * kBN;
                     a_k0 = b_k0 = 0;
                 } else if (un.type == kUnitDH) {
-                    wait_at_least(p.counters + p.gm_base + un.c * p.mb_max + un.m_blk, ck.vt);
-                    if (ck.band_idx > 0) wait_at_least(ctr + 1 + 4 * (un.c - 1) + 1, p.chunks[un.c - 1].n_dh);
-                    kbs = (ck.vc + kBK - 1) / kBK;
+                    wait_at_least(p.counters + p.gm_base + un.c * p.mb_max + un.m_blk, p.vt);
+                    if (un.band_idx > 0) wait_at_least(cnt(p, un.c - 1, 1), p.n_dh);
                     ma = &maps.g_k;
                     mb = &maps.w_mn;
                     a_mn = 0;
                     b_mn = 1;
-                    a_row = ck.slot * p.nc_max + un.m_blk * kBM;
+                    a_row = un.slot * p.nc_max + un.m_blk * kBM;
                     b_row = un.n_tile * kBN;
                     a_k0 = 0;
-                    b_k0 = ck.vb;
+                    b_k0 = un.vb;
                     pa = pol_g;
                 } else {
-                    wait_at_least(cc + 0, ck.n_g);
-                    if (ck.row_idx > 0) wait_at_least(ctr + 1 + 4 * (un.c - p.bands) + 2, p.chunks[un.c - p.bands].n_dw);
-                    kbs = (ck.nc + kBK - 1) / kBK;
+                    wait_at_least(cnt(p, un.c, 0), p.n_g);
+                    if (un.row_idx > 0) wait_at_least(cnt(p, un.c - p.bands, 2), p.n_dw);
                     ma = &maps.g_mn;
                     mb = &maps.h_mn;
-                    a_mn = 1;
-                    b_mn = 1;
+                    a_mn = b_mn = 1;
                     a_row = un.m_blk * kBM;
                     b_row = un.n_tile * kBN;
-                    a_k0 = ck.slot * p.nc_max;
-                    b_k0 = ck.r0;
+                    a_k0 = un.slot * p.nc_max;
+                    b_k0 = un.r0;
                     pa = pol_g;
                     pb = pol_h;
                 }
-                // order the acquire above before this thread's async-proxy (TMA) reads
+                // order the acquires above before this thread's async-proxy (TMA) reads
                 fence_proxy_async_global();
+                const int kbs = unit_kblocks(p, un);
                 for (int kb = 0; kb < kbs; ++kb) {
                     mbar_wait(&empty[stage], phase ^ 1);
                     mbar_arrive_expect_tx(&full[stage], kStageBytesA + kStageBytesB);
@@ -259,22 +276,11 @@ __global__ void __launch_bounds__(kThreads, 1)
                 }
                 const BUnit un = decode_unit(p, u);
                 if (un.type == kUnitStop) break;
-                const BwdChunk ck = p.chunks[un.c];
-                int kbs, a_mn, b_mn;
-                if (un.type == kUnitGrad) {
-                    kbs = p.k_blocks_d;
-                    a_mn = 0;
-                    b_mn = 0;
-                } else if (un.type == kUnitDH) {
-                    kbs = (ck.vc + kBK - 1) / kBK;
-                    a_mn = 0;
-                    b_mn = 1;
-                } else {
-                    kbs = (ck.nc + kBK - 1) / kBK;
-                    a_mn = 1;
-                    b_mn = 1;
-                }
+                if (un.empty) continue;
+                const int a_mn = un.type == kUnitDW ? 1 : 0;
+                const int b_mn = un.type == kUnitGrad ? 0 : 1;
                 const uint32_t idesc = make_idesc_bf16(kBM, kBN, a_mn, b_mn);
+                const int kbs = unit_kblocks(p, un);
                 mbar_wait(&tempty[acc], acc_phase ^ 1);
                 tc_fence_after();
                 const uint32_t d_tmem = tmem_base + acc * kBN;
@@ -321,111 +327,112 @@ __global__ void __launch_bounds__(kThreads, 1)
             }
             const BUnit un = decode_unit(p, u);
             if (un.type == kUnitStop) break;
-            const BwdChunk ck = p.chunks[un.c];
 
-            mbar_wait(&tfull[acc], acc_phase);
-            tc_fence_after();
-            const uint32_t taddr = tmem_base + (static_cast<uint32_t>(q * 32) << 16) +
-                                   static_cast<uint32_t>(acc * kBN);
-            if (un.type == kUnitGrad) {
-                const int lrow = un.m_blk * kBM + r;  // row inside the chunk
-                const bool row_ok = lrow < ck.nc;
-                const int64_t grow = static_cast<int64_t>(ck.r0) + lrow;
-                float gam = 0.f, l2lse = 0.f;
-                int64_t tcol = -1;
-                if (row_ok) {
-                    const int64_t y = p.targets[grow];
-                    const bool skip = p.has_ignore && y == p.ignore_index;
-                    gam = skip ? 0.f : p.gamma[grow];
-                    l2lse = skip ? 0.f : p.lse[grow] * kL2e;
-                    tcol = y - (p.v_offset + ck.vb);
-                }
-                __nv_bfloat16* grow_ptr =
-                    p.g_ring + (static_cast<int64_t>(ck.slot) * p.nc_max + lrow) * p.ldg;
-#pragma unroll 1
-                for (int c = 0; c < kBN / 32; ++c) {
-                    float v[32];
-                    tmem_ld32(taddr + c * 32, v);
-                    const int col0 = un.n_tile * kBN + c * 32;
+            if (!un.empty) {
+                mbar_wait(&tfull[acc], acc_phase);
+                tc_fence_after();
+                const uint32_t taddr = tmem_base + (static_cast<uint32_t>(q * 32) << 16) +
+                                       static_cast<uint32_t>(acc * kBN);
+                if (un.type == kUnitGrad) {
+                    const int lrow = un.m_blk * kBM + r;  // row inside the chunk
+                    const bool row_ok = lrow < un.nc;
+                    const int64_t grow = static_cast<int64_t>(un.r0) + lrow;
+                    float gam = 0.f, l2lse = 0.f;
+                    int64_t tcol = -1;
                     if (row_ok) {
-                        const int64_t tc = tcol - col0;
-                        uint32_t packed[16];
-#pragma unroll
-                        for (int j = 0; j < 32; j += 2) {
-                            float g0 = gam * (ex2(fmaf(v[j], kL2e, -l2lse)) - (tc == j ? 1.f : 0.f));
-                            float g1 = gam * (ex2(fmaf(v[j + 1], kL2e, -l2lse)) - (tc == j + 1 ? 1.f : 0.f));
-                            if (gam == 0.f || col0 + j >= ck.vc) g0 = 0.f;
-                            if (gam == 0.f || col0 + j + 1 >= ck.vc) g1 = 0.f;
-                            packed[j >> 1] = pack_bf16(g0, g1);
-                        }
-                        __nv_bfloat16* dst = grow_ptr + col0;
-#pragma unroll
-                        for (int j = 0; j < 4; ++j)
-                            st_v4_b32_hint(dst + 8 * j, packed[4 * j], packed[4 * j + 1], packed[4 * j + 2],
-                                           packed[4 * j + 3], pol_gst);
+                        const int64_t y = p.targets[grow];
+                        const bool skip = p.has_ignore && y == p.ignore_index;
+                        gam = skip ? 0.f : p.gamma[grow];
+                        l2lse = skip ? 0.f : p.lse[grow] * kL2e;
+                        tcol = y - (p.v_offset + un.vb);
                     }
-                }
-            } else {
-                // dH: rows = chunk rows, C = dH + (r0 + row) * lddh; dW: rows = band vocab rows
-                const bool is_dh = un.type == kUnitDH;
-                const int lrow = un.m_blk * kBM + r;
-                const int mrows = is_dh ? ck.nc : ck.vc;
-                const bool accumulate = is_dh ? (ck.band_idx > 0 || p.accumulate_dh) : (ck.row_idx > 0);
-                float* crow = is_dh ? p.dh + (static_cast<int64_t>(ck.r0) + lrow) * p.lddh
-                                    : p.dw + (static_cast<int64_t>(ck.vb) + lrow) * p.lddw;
+                    __nv_bfloat16* grow_ptr =
+                        p.g_ring + (static_cast<int64_t>(un.slot) * p.nc_max + lrow) * p.ldg;
 #pragma unroll 1
-                for (int c = 0; c < kBN / 32; ++c) {
-                    float v[32];
-                    tmem_ld32(taddr + c * 32, v);
-                    const int col0 = un.n_tile * kBN + c * 32;
-                    if (lrow < mrows) {
-                        float* dst = crow + col0;
-                        const bool vec = (col0 + 32 <= p.d) && ((reinterpret_cast<uintptr_t>(dst) & 15) == 0);
-                        if (vec) {
-                            if (accumulate) {
+                    for (int c = 0; c < kBN / 32; ++c) {
+                        float v[32];
+                        tmem_ld32(taddr + c * 32, v);
+                        const int col0 = un.n_tile * kBN + c * 32;
+                        if (row_ok) {
+                            const int64_t tc = tcol - col0;
+                            uint32_t packed[16];
 #pragma unroll
-                                for (int j = 0; j < 32; j += 4)
-                                    red_add_v4_hint(dst + j, v[j], v[j + 1], v[j + 2], v[j + 3], pol_out);
-                            } else {
-#pragma unroll
-                                for (int j = 0; j < 32; j += 4)
-                                    st_v4_hint(dst + j, v[j], v[j + 1], v[j + 2], v[j + 3], pol_out);
+                            for (int j = 0; j < 32; j += 2) {
+                                float g0 = gam * (ex2(fmaf(v[j], kL2e, -l2lse)) - (tc == j ? 1.f : 0.f));
+                                float g1 = gam * (ex2(fmaf(v[j + 1], kL2e, -l2lse)) - (tc == j + 1 ? 1.f : 0.f));
+                                if (gam == 0.f || col0 + j >= un.vc) g0 = 0.f;
+                                if (gam == 0.f || col0 + j + 1 >= un.vc) g1 = 0.f;
+                                packed[j >> 1] = pack_bf16(g0, g1);
                             }
-                        } else {
-                            for (int j = 0; j < 32; ++j) {
-                                if (col0 + j < p.d) {
-                                    if (accumulate)
-                                        atomicAdd(dst + j, v[j]);
-                                    else
-                                        dst[j] = v[j];
+                            __nv_bfloat16* dst = grow_ptr + col0;
+#pragma unroll
+                            for (int j = 0; j < 4; ++j)
+                                st_v4_b32_hint(dst + 8 * j, packed[4 * j], packed[4 * j + 1],
+                                               packed[4 * j + 2], packed[4 * j + 3], pol_gst);
+                        }
+                    }
+                } else {
+                    // dH rows = chunk rows into dH; dW rows = band vocab rows into dW
+                    const bool is_dh = un.type == kUnitDH;
+                    const int lrow = un.m_blk * kBM + r;
+                    const int mrows = is_dh ? un.nc : un.vc;
+                    const bool accumulate = is_dh ? (un.band_idx > 0 || p.accumulate_dh) : (un.row_idx > 0);
+                    float* crow = is_dh ? p.dh + (static_cast<int64_t>(un.r0) + lrow) * p.lddh
+                                        : p.dw + (static_cast<int64_t>(un.vb) + lrow) * p.lddw;
+#pragma unroll 1
+                    for (int c = 0; c < kBN / 32; ++c) {
+                        float v[32];
+                        tmem_ld32(taddr + c * 32, v);
+                        const int col0 = un.n_tile * kBN + c * 32;
+                        if (lrow < mrows) {
+                            float* dst = crow + col0;
+                            const bool vec = (col0 + 32 <= p.d) && ((reinterpret_cast<uintptr_t>(dst) & 15) == 0);
+                            if (vec) {
+                                if (accumulate) {
+#pragma unroll
+                                    for (int j = 0; j < 32; j += 4)
+                                        red_add_v4_hint(dst + j, v[j], v[j + 1], v[j + 2], v[j + 3], pol_out);
+                                } else {
+#pragma unroll
+                                    for (int j = 0; j < 32; j += 4)
+                                        st_v4_hint(dst + j, v[j], v[j + 1], v[j + 2], v[j + 3], pol_out);
+                                }
+                            } else {
+                                for (int j = 0; j < 32; ++j) {
+                                    if (col0 + j < p.d) {
+                                        if (accumulate)
+                                            atomicAdd(dst + j, v[j]);
+                                        else
+                                            dst[j] = v[j];
+                                    }
                                 }
                             }
                         }
                     }
                 }
+                tc_fence_before();
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&tempty[acc]);
+                acc ^= 1;
+                if (acc == 0) acc_phase ^= 1;
+                // generic-proxy stores above are read later through TMA (async proxy)
+                fence_proxy_async_global();
             }
-            tc_fence_before();
-            __syncwarp();
-            if (lane == 0) mbar_arrive(&tempty[acc]);
-            acc ^= 1;
-            if (acc == 0) acc_phase ^= 1;
 
-            // publish completion of this unit: all 128 epilogue threads' stores,
-            // then one gpu-scope release
-            fence_proxy_async_global();
+            // publish completion: all 128 epilogue threads' stores, then one
+            // gpu-scope release
             named_bar_sync(1, 128);
             if (threadIdx.x == 128) {
                 __threadfence();
-                unsigned* cc = ctr + 1 + 4 * un.c;
                 if (un.type == kUnitGrad) {
-                    atomicAdd(ctr + p.gm_base + un.c * p.mb_max + un.m_blk, 1u);
-                    atomicAdd(cc + 0, 1u);
+                    atomicAdd(p.counters + p.gm_base + un.c * p.mb_max + un.m_blk, 1u);
+                    atomicAdd(cnt(p, un.c, 0), 1u);
                 } else if (un.type == kUnitDH) {
-                    atomicAdd(cc + 1, 1u);
-                    atomicAdd(cc + 3, 1u);
+                    atomicAdd(cnt(p, un.c, 1), 1u);
+                    atomicAdd(cnt(p, un.c, 3), 1u);
                 } else {
-                    atomicAdd(cc + 2, 1u);
-                    atomicAdd(cc + 3, 1u);
+                    atomicAdd(cnt(p, un.c, 2), 1u);
+                    atomicAdd(cnt(p, un.c, 3), 1u);
                 }
             }
         }

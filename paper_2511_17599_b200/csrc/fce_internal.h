@@ -67,24 +67,19 @@ struct TensorMaps {
 };
 
 // ----------------------------------------------------------- persistent backward
-// One (row chunk x vocab band) chunk of the backward (fce_bwd.cu).
-struct BwdChunk {
-    int r0, nc;          // rows [r0, r0 + nc)
-    int vb, vc;          // local vocab rows [vb, vb + vc)
-    int slot;            // G ring slot
-    int row_idx, band_idx;
-    int vt, vm;          // vocab tiles of 256 (grad units per m-block) / of 128 (dW rows)
-    int n_g, n_dh, n_dw; // unit counts
-};
-
+// Every (row chunk x vocab band) chunk is laid out at full geometry; see fce_bwd.cu.
 struct BwdParams {
-    int units, n_chunks, bands, d_tiles, k_blocks_d, mb_max, gm_base;
+    int units;               // n_chunks * per_chunk
+    int n_chunks, bands;     // chunks = row chunks x bands, chunk c = (c / bands, c % bands)
+    int per_chunk;           // n_g + n_dh + n_dw
+    int n_g, n_dh, n_dw;     // grad / dH / dW units per chunk (padded geometry)
+    int vt, vm;              // band / 256, band / 128
+    int d_tiles, k_blocks_d, mb_max, gm_base;
+    int n, v;                // rows, local vocab rows
     int has_ignore, accumulate_dh;
     int l2_hints;            // bit0: evict_first on dH/dW writes, bit1: evict_last on G loads,
                              // bit2: evict_last on G stores, bit3: evict_first on H loads (dW)
     int64_t nc_max, ldg, d, lddh, lddw, v_offset, ignore_index;
-    const BwdChunk* chunks;
-    const int* bnd;          // 2 * n_chunks + 1 segment boundaries
     unsigned* counters;      // [0] scheduler, 4 per chunk, then mb_max per chunk
     const int64_t* targets;
     const float* lse;
