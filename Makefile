@@ -17,9 +17,9 @@ REF_LIB   := oracle/_ref/libfce_ref.so
 
 all: $(LIB) $(ORACLE) ref
 
-$(LIB): $(CSRC)/fce_kernels.cu $(CSRC)/fce_bwd.cu $(CSRC)/fce_api.cpp $(CSRC)/fce_vp.cpp $(CSRC)/fce_internal.h \
+$(LIB): $(CSRC)/fce_kernels.cu $(CSRC)/fce_bwd.cu $(CSRC)/fce_pair.cu $(CSRC)/fce_api.cpp $(CSRC)/fce_vp.cpp $(CSRC)/fce_internal.h \
         $(CSRC)/sm100_ptx.cuh include/fce/fce.h
-	$(NVCC) $(NVFLAGS) -shared -cudart static -o $@ $(CSRC)/fce_kernels.cu $(CSRC)/fce_bwd.cu $(CSRC)/fce_api.cpp \
+	$(NVCC) $(NVFLAGS) -shared -cudart static -o $@ $(CSRC)/fce_kernels.cu $(CSRC)/fce_bwd.cu $(CSRC)/fce_pair.cu $(CSRC)/fce_api.cpp \
 	    $(CSRC)/fce_vp.cpp -ldl -lpthread -lrt
 
 $(ORACLE): oracle/fce_oracle.c oracle/fce_oracle.h

@@ -54,6 +54,7 @@ struct fce_handle_s {
     int* host_err = nullptr;                // pinned mirror
     int64_t splits = 0, band_cols = 0, row_chunk = 0, validate = 1, bwd_persistent = 1;
     int64_t l2_hints = 1;
+    int64_t gemm_pair = 1;
     int64_t launches = 0;
     size_t bwd_scratch[4] = {0, 0, 0, 0};  // offsets of the persistent-backward scratch
     // optional per-kernel CUDA-event timing of the tile kernels (bench roofline)
@@ -442,6 +443,8 @@ fce_status fce_set_option(fce_handle h, const char* key, int64_t value) {
         h->row_chunk = value;
     } else if (!std::strcmp(key, "validate")) {
         h->validate = value ? 1 : 0;
+    } else if (!std::strcmp(key, "gemm_pair")) {
+        h->gemm_pair = value ? 1 : 0;
     } else if (!std::strcmp(key, "l2_hints")) {
         h->l2_hints = value;
     } else if (!std::strcmp(key, "bwd_persistent")) {
@@ -758,7 +761,7 @@ fce_status fce_gemm_bf16(fce_handle h, const void* a, int64_t lda, int a_mn, con
     const bool ok_a = a_mn ? encode_map_2d(&gm.a0, a, m, k, lda * 2, 64, 64)
                            : encode_map_2d(&gm.a0, a, k, m, lda * 2, kBK, kBM);
     const bool ok_b = b_mn ? encode_map_2d(&gm.b0, b, n, k, ldb * 2, 64, 64)
-                           : encode_map_2d(&gm.b0, b, k, n, ldb * 2, kBK, kBN);
+                           : encode_map_2d(&gm.b0, b, k, n, ldb * 2, kBK, h->gemm_pair ? 128 : kBN);
     if (!ok_a || !ok_b) return fail(FCE_CUDA_ERROR, "cuTensorMapEncodeTiled failed (gemm)");
     GemmProblem& q = gp.prob[0];
     q.m = static_cast<int>(m);
@@ -775,7 +778,13 @@ fce_status fce_gemm_bf16(fce_handle h, const void* a, int64_t lda, int a_mn, con
     gp.mode = kEpiGemm;
     gp.units0 = q.m_tiles * q.n_tiles;
     gp.units = gp.units0;
-    cudaError_t e = timed_launch(h, gp, gm, 2.0 * m * n * k);
+    cudaError_t e;
+    if (h->gemm_pair) {
+        e = launch_pair_gemm(q, gm, h->sms, h->stream);
+        h->launches += 1;
+    } else {
+        e = timed_launch(h, gp, gm, 2.0 * m * n * k);
+    }
     if (e != cudaSuccess) return fail(FCE_CUDA_ERROR, "gemm tile kernel: %s", cudaGetErrorString(e));
     return FCE_OK;
 }

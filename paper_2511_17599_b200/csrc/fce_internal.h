@@ -93,6 +93,9 @@ struct BwdMaps {
     CUtensorMap h_k, w_k, g_k, w_mn, g_mn, h_mn;
 };
 
+cudaError_t launch_pair_gemm(const GemmProblem& q, const TensorMaps& maps, int sms,
+                             cudaStream_t stream);
+
 cudaError_t launch_bwd_persistent(const BwdParams& p, const BwdMaps& maps, int grid,
                                   cudaStream_t stream);
 
