@@ -277,14 +277,14 @@ fce_status run_backward_persistent(fce_handle h, const fce_problem* p, const flo
 
     const int64_t n_rc = ceil_div(p->n, row_chunk), n_bd = ceil_div(p->v, band);
     const int64_t n_chunks = n_rc * n_bd;
-    const int mb_max = static_cast<int>(row_chunk / kBM);
+    const int mb_max = static_cast<int>(row_chunk / 256);  // 256-row pair units
     const int d_tiles = static_cast<int>(ceil_div(p->d, kBN));
     BwdParams bp;
     std::memset(&bp, 0, sizeof(bp));
     bp.n_chunks = static_cast<int>(n_chunks);
     bp.bands = static_cast<int>(n_bd);
     bp.vt = static_cast<int>(band / kBN);
-    bp.vm = static_cast<int>(band / kBM);
+    bp.vm = static_cast<int>(band / 256);
     bp.n_g = mb_max * bp.vt;
     bp.n_dh = dhidden ? mb_max * d_tiles : 0;
     bp.n_dw = dweight ? bp.vm * d_tiles : 0;
@@ -324,9 +324,10 @@ fce_status run_backward_persistent(fce_handle h, const fce_problem* p, const flo
     BwdMaps maps;
     std::memset(&maps, 0, sizeof(maps));
     const uint64_t ring_rows = static_cast<uint64_t>(2 * row_chunk);
-    if (!encode_map_2d(&maps.h_k, p->hidden, p->d, p->n, p->ldh * 2, kBK, kBM) ||
-        !encode_map_2d(&maps.w_k, p->weight, p->d, p->v, p->ldw * 2, kBK, kBN) ||
-        !encode_map_2d(&maps.g_k, g_ring, band, ring_rows, band * 2, kBK, kBM) ||
+    // pair units: every CTA loads 128 rows of K-major operands per stage
+    if (!encode_map_2d(&maps.h_k, p->hidden, p->d, p->n, p->ldh * 2, kBK, 128) ||
+        !encode_map_2d(&maps.w_k, p->weight, p->d, p->v, p->ldw * 2, kBK, 128) ||
+        !encode_map_2d(&maps.g_k, g_ring, band, ring_rows, band * 2, kBK, 128) ||
         !encode_map_2d(&maps.w_mn, p->weight, p->d, p->v, p->ldw * 2, 64, 64) ||
         !encode_map_2d(&maps.g_mn, g_ring, band, ring_rows, band * 2, 64, 64) ||
         !encode_map_2d(&maps.h_mn, p->hidden, p->d, p->n, p->ldh * 2, 64, 64))
@@ -613,7 +614,8 @@ fce_status fce_backward(fce_handle h, const fce_problem* p, fce_stats stats, int
 
     // chunking of G = N_c x V_c bf16
     int64_t row_chunk = h->row_chunk ? h->row_chunk : 8192;
-    row_chunk = std::min(row_chunk, round_up(p->n, kBM));
+    row_chunk = std::min(row_chunk, round_up(p->n, h->bwd_persistent ? 256 : kBM));
+    if (h->bwd_persistent) row_chunk = round_up(row_chunk, 256);
     int64_t band = h->band_cols;
     if (!band) {
         // ~32 MB of G per chunk so it stays L2 resident between producer and consumers
@@ -627,7 +629,7 @@ fce_status fce_backward(fce_handle h, const fce_problem* p, fce_stats stats, int
     const size_t o_G = sc.take(sizeof(__nv_bfloat16) * row_chunk * band * (h->bwd_persistent ? 2 : 1));
     const int64_t n_rc = ceil_div(p->n, row_chunk), n_bd = ceil_div(p->v, band);
     const int64_t n_chunks = n_rc * n_bd;
-    const int64_t mb_max = ceil_div(row_chunk, kBM);
+    const int64_t mb_max = ceil_div(row_chunk, 128);
     const size_t o_tab = 0, o_bnd = 0;
     const size_t o_ctr = sc.take(sizeof(unsigned) * (1 + 4 * n_chunks + n_chunks * mb_max));
     if ((s = sc.commit())) return s;

@@ -9,11 +9,15 @@
 // G = gamma (softmax - onehot), bf16, moves between them through a 2-slot ring
 // of (row chunk x vocab band) chunks sized to stay L2-resident.
 //
+// Execution: CTA pairs (cluster of 2, tcgen05.mma.cta_group::2, M = 256): each
+// CTA loads its 128 rows of A and its 128 columns of B per 64-deep K stage
+// (32 KB, 6 stages), the even CTA issues the MMAs for both, and each CTA's
+// epilogue drains its own 128 accumulator rows.  A unit is a 256 x 256 tile.
 // Work units of one launch, dispatched in this order by an atomic counter
-// (work stealing, 1 CTA per SM):
+// (work stealing per pair):
 //     G(0) M(0) G(1) M(1) ... G(C-1) M(C-1)
-//   G(c): 128x256 S tiles of chunk c -> G tile into ring slot c % 2
-//   M(c): dH units (128 rows x 256 d, K = band) then dW units (128 vocab rows
+//   G(c): 256x256 S tiles of chunk c -> G tile into ring slot c % 2
+//   M(c): dH units (256 rows x 256 d, K = band) then dW units (256 vocab rows
 //         x 256 d, K = row chunk) reading ring slot c % 2
 // Every chunk is counted at full (row_chunk x band) geometry so a unit index
 // decodes with two divisions; units that fall past N or V in the last row
@@ -38,13 +42,17 @@ using namespace ptx;
 
 static constexpr float kL2e = 1.4426950408889634f;
 constexpr int kUnitRing = 4;
+constexpr int kPS = 6;                     // pipeline stages
+constexpr int kPA = 128 * kBK * 2;         // this CTA's A rows per stage
+constexpr int kPB = 128 * kBK * 2;         // this CTA's B columns per stage
+constexpr int kPM = 256;                   // unit rows (pair)
 
 enum UnitType : int { kUnitGrad = 0, kUnitDH = 1, kUnitDW = 2, kUnitStop = 3 };
 
 struct BUnit {
     int type;     // UnitType
     int c;        // chunk
-    int m_blk;    // 128-row block: chunk rows (grad, dH) or band vocab rows (dW)
+    int m_blk;    // 256-row block: chunk rows (grad, dH) or band vocab rows (dW)
     int n_tile;   // 256-wide tile: band vocab (grad) or d (dH, dW)
     int r0, nc;   // chunk rows [r0, r0 + nc)
     int vb, vc;   // band vocab rows [vb, vb + vc)
@@ -73,19 +81,19 @@ __device__ __forceinline__ BUnit decode_unit(const BwdParams& p, int u) {
         r.type = kUnitGrad;
         r.m_blk = l / p.vt;
         r.n_tile = l - r.m_blk * p.vt;
-        r.empty = r.m_blk * kBM >= r.nc || r.n_tile * kBN >= r.vc;
+        r.empty = r.m_blk * kPM >= r.nc || r.n_tile * kBN >= r.vc;
     } else if (l < p.n_g + p.n_dh) {
         const int l2 = l - p.n_g;
         r.type = kUnitDH;
         r.m_blk = l2 / p.d_tiles;
         r.n_tile = l2 - r.m_blk * p.d_tiles;
-        r.empty = r.m_blk * kBM >= r.nc;
+        r.empty = r.m_blk * kPM >= r.nc;
     } else {
         const int l2 = l - p.n_g - p.n_dh;
         r.type = kUnitDW;
         r.n_tile = l2 / p.vm;
         r.m_blk = l2 - r.n_tile * p.vm;
-        r.empty = r.m_blk * kBM >= r.vc;
+        r.empty = r.m_blk * kPM >= r.vc;
     }
     return r;
 }
@@ -110,7 +118,8 @@ __device__ __forceinline__ void named_bar_sync(int id, int count) {
 }
 
 // counters: [0] scheduler; chunk c: [1+4c] G done, [2+4c] dH done, [3+4c] dW done,
-// [4+4c] M (dH + dW) done; then per (chunk, 128-row block) G done.
+// [4+4c] M (dH + dW) done; then per (chunk, 256-row block) G done.  Both CTAs
+// of a pair signal every unit, so every target is twice the unit count.
 __device__ __forceinline__ unsigned* cnt(const BwdParams& p, int c, int k) {
     return p.counters + 1 + 4 * c + k;
 }
@@ -121,17 +130,17 @@ __device__ __forceinline__ int unit_kblocks(const BwdParams& p, const BUnit& un)
     return (un.nc + kBK - 1) / kBK;
 }
 
-__global__ void __launch_bounds__(kThreads, 1)
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     fce_bwd_persistent_kernel(const __grid_constant__ BwdParams p, const __grid_constant__ BwdMaps maps) {
     extern __shared__ uint8_t smem_raw[];
     const uint32_t raw_addr = smem_u32(smem_raw);
     uint8_t* smem = smem_raw + (((raw_addr + 1023u) & ~1023u) - raw_addr);
     uint8_t* sA = smem;
-    uint8_t* sB = smem + kStages * kStageBytesA;
-    uint64_t* bars = reinterpret_cast<uint64_t*>(sB + kStages * kStageBytesB);
+    uint8_t* sB = smem + kPS * kPA;
+    uint64_t* bars = reinterpret_cast<uint64_t*>(sB + kPS * kPB);
     uint64_t* full = bars;
-    uint64_t* empty = bars + kStages;
-    uint64_t* tfull = bars + 2 * kStages;
+    uint64_t* empty = bars + kPS;
+    uint64_t* tfull = bars + 2 * kPS;
     uint64_t* tempty = tfull + 2;
     uint64_t* ufull = tempty + 2;
     uint64_t* uempty = ufull + kUnitRing;
@@ -140,19 +149,22 @@ __global__ void __launch_bounds__(kThreads, 1)
 
     const int warp = threadIdx.x >> 5;
     const int lane = threadIdx.x & 31;
+    const uint32_t rank = cluster_ctarank();
+    const unsigned two = 2u;  // signals per unit (one per CTA of the pair)
 
     if (threadIdx.x == 0) {
-        for (int s = 0; s < kStages; ++s) {
+        for (int s = 0; s < kPS; ++s) {
             mbar_init(&full[s], 1);
             mbar_init(&empty[s], 1);
         }
         for (int b = 0; b < 2; ++b) {
             mbar_init(&tfull[b], 1);
-            mbar_init(&tempty[b], 4);
+            mbar_init(&tempty[b], 8);  // 4 epilogue warps x 2 CTAs (leader's copy)
         }
         for (int s = 0; s < kUnitRing; ++s) {
             mbar_init(&ufull[s], 1);
-            mbar_init(&uempty[s], 5);  // MMA thread + one lane of each epilogue warp
+            // leader's copy: MMA thread + 4 epilogue warps of each CTA + peer producer
+            mbar_init(&uempty[s], 10);
         }
         fence_mbar_init();
     }
@@ -164,11 +176,12 @@ __global__ void __launch_bounds__(kThreads, 1)
         tma_prefetch_desc(&maps.g_mn);
         tma_prefetch_desc(&maps.h_mn);
     }
-    if (warp == 2) tmem_alloc<512>(tmem_slot);
+    if (warp == 2) tmem_alloc_pair<512>(tmem_slot);
     tc_fence_before();
-    __syncthreads();
+    cluster_sync_all();
     tc_fence_after();
     const uint32_t tmem_base = *tmem_slot;
+    const uint32_t leader_uempty0 = mapa_shared(&uempty[0], 0);
 
     if (warp == 0) {
         // ------------------------------------------------ scheduler + TMA producer
@@ -178,54 +191,67 @@ __global__ void __launch_bounds__(kThreads, 1)
             const uint64_t pol_norm = policy_evict_normal();
             const uint64_t pol_g = (p.l2_hints & 2) ? policy_evict_last() : pol_norm;
             const uint64_t pol_h = (p.l2_hints & 8) ? policy_evict_first() : pol_norm;
-            int u_next = static_cast<int>(atomicAdd(p.counters, 1u));
+            const uint32_t leader_full0 = mapa_shared(&full[0], 0);
+            const uint32_t peer_ring0 = mapa_shared(&unit_ring[0], 1);
+            const uint32_t peer_ufull0 = mapa_shared(&ufull[0], 1);
+            int u_next = rank == 0 ? static_cast<int>(atomicAdd(p.counters, 1u)) : 0;
             for (;;) {
-                const int u = u_next;
-                const BUnit un = decode_unit(p, u);
-                mbar_wait(&uempty[us], uphase ^ 1);
-                unit_ring[us] = u;
-                mbar_arrive(&ufull[us]);
+                int u;
+                if (rank == 0) {
+                    // publish the unit to both CTAs of the pair
+                    u = u_next;
+                    mbar_wait_cluster(&uempty[us], uphase ^ 1);
+                    unit_ring[us] = u;
+                    st_shared_cluster_u32(peer_ring0 + 4 * us, static_cast<uint32_t>(u));
+                    mbar_arrive(&ufull[us]);
+                    mbar_arrive_cluster(peer_ufull0 + 8 * us);
+                } else {
+                    mbar_wait_cluster(&ufull[us], uphase);
+                    u = unit_ring[us];
+                    mbar_arrive_cluster(leader_uempty0 + 8 * us);
+                }
                 if (++us == kUnitRing) {
                     us = 0;
                     uphase ^= 1;
                 }
+                const BUnit un = decode_unit(p, u);
                 if (un.type == kUnitStop) break;
                 // claim the next unit now; the atomic's latency hides behind this
                 // unit's loads (its result is first used at the top of the loop)
-                u_next = static_cast<int>(atomicAdd(p.counters, 1u));
+                if (rank == 0) u_next = static_cast<int>(atomicAdd(p.counters, 1u));
                 if (un.empty) continue;
                 const CUtensorMap *ma, *mb;
                 int a_mn, b_mn, a_row, b_row, a_k0, b_k0;
                 uint64_t pa = pol_norm, pb = pol_norm;
                 if (un.type == kUnitGrad) {
-                    if (un.c >= 2) wait_at_least(cnt(p, un.c - 2, 3), p.n_dh + p.n_dw);
+                    if (un.c >= 2) wait_at_least(cnt(p, un.c - 2, 3), two * (p.n_dh + p.n_dw));
                     ma = &maps.h_k;
                     mb = &maps.w_k;
                     a_mn = b_mn = 0;
-                    a_row = un.r0 + un.m_blk * kBM;
-                    b_row = un.vb + un.n_tile * kBN;
+                    a_row = un.r0 + un.m_blk * kPM + rank * 128;
+                    b_row = un.vb + un.n_tile * kBN + rank * 128;
                     a_k0 = b_k0 = 0;
                 } else if (un.type == kUnitDH) {
-                    wait_at_least(p.counters + p.gm_base + un.c * p.mb_max + un.m_blk, p.vt);
-                    if (un.band_idx > 0) wait_at_least(cnt(p, un.c - 1, 1), p.n_dh);
+                    wait_at_least(p.counters + p.gm_base + un.c * p.mb_max + un.m_blk, two * p.vt);
+                    if (un.band_idx > 0) wait_at_least(cnt(p, un.c - 1, 1), two * p.n_dh);
                     ma = &maps.g_k;
                     mb = &maps.w_mn;
                     a_mn = 0;
                     b_mn = 1;
-                    a_row = un.slot * p.nc_max + un.m_blk * kBM;
-                    b_row = un.n_tile * kBN;
+                    a_row = un.slot * static_cast<int>(p.nc_max) + un.m_blk * kPM + rank * 128;
+                    b_row = un.n_tile * kBN + rank * 128;
                     a_k0 = 0;
                     b_k0 = un.vb;
                     pa = pol_g;
                 } else {
-                    wait_at_least(cnt(p, un.c, 0), p.n_g);
-                    if (un.row_idx > 0) wait_at_least(cnt(p, un.c - p.bands, 2), p.n_dw);
+                    wait_at_least(cnt(p, un.c, 0), two * p.n_g);
+                    if (un.row_idx > 0) wait_at_least(cnt(p, un.c - p.bands, 2), two * p.n_dw);
                     ma = &maps.g_mn;
                     mb = &maps.h_mn;
                     a_mn = b_mn = 1;
-                    a_row = un.m_blk * kBM;
-                    b_row = un.n_tile * kBN;
-                    a_k0 = un.slot * p.nc_max;
+                    a_row = un.m_blk * kPM + rank * 128;
+                    b_row = un.n_tile * kBN + rank * 128;
+                    a_k0 = un.slot * static_cast<int>(p.nc_max);
                     b_k0 = un.r0;
                     pa = pol_g;
                     pb = pol_h;
@@ -235,26 +261,25 @@ __global__ void __launch_bounds__(kThreads, 1)
                 const int kbs = unit_kblocks(p, un);
                 for (int kb = 0; kb < kbs; ++kb) {
                     mbar_wait(&empty[stage], phase ^ 1);
-                    mbar_arrive_expect_tx(&full[stage], kStageBytesA + kStageBytesB);
-                    uint8_t* a_dst = sA + stage * kStageBytesA;
-                    uint8_t* b_dst = sB + stage * kStageBytesB;
+                    if (rank == 0) mbar_arrive_expect_tx(&full[stage], 2 * (kPA + kPB));
+                    const uint32_t fb = leader_full0 + stage * 8;
+                    uint8_t* a_dst = sA + stage * kPA;
+                    uint8_t* b_dst = sB + stage * kPB;
                     if (!a_mn) {
-                        tma_load_2d(a_dst, ma, &full[stage], a_k0 + kb * kBK, a_row, pa);
+                        tma_load_2d_pair(a_dst, ma, fb, a_k0 + kb * kBK, a_row, pa);
                     } else {
 #pragma unroll
-                        for (int j = 0; j < kBM / 64; ++j)
-                            tma_load_2d(a_dst + j * 8192, ma, &full[stage], a_row + 64 * j,
-                                        a_k0 + kb * kBK, pa);
+                        for (int j = 0; j < 2; ++j)
+                            tma_load_2d_pair(a_dst + j * 8192, ma, fb, a_row + 64 * j, a_k0 + kb * kBK, pa);
                     }
                     if (!b_mn) {
-                        tma_load_2d(b_dst, mb, &full[stage], b_k0 + kb * kBK, b_row, pb);
+                        tma_load_2d_pair(b_dst, mb, fb, b_k0 + kb * kBK, b_row, pb);
                     } else {
 #pragma unroll
-                        for (int j = 0; j < kBN / 64; ++j)
-                            tma_load_2d(b_dst + j * 8192, mb, &full[stage], b_row + 64 * j,
-                                        b_k0 + kb * kBK, pb);
+                        for (int j = 0; j < 2; ++j)
+                            tma_load_2d_pair(b_dst + j * 8192, mb, fb, b_row + 64 * j, b_k0 + kb * kBK, pb);
                     }
-                    if (++stage == kStages) {
+                    if (++stage == kPS) {
                         stage = 0;
                         phase ^= 1;
                     }
@@ -262,8 +287,8 @@ __global__ void __launch_bounds__(kThreads, 1)
             }
         }
     } else if (warp == 1) {
-        // ------------------------------------------------ MMA issuer
-        if (lane == 0) {
+        // ------------------------------------------------ MMA issuer (even CTA)
+        if (lane == 0 && rank == 0) {
             int stage = 0, us = 0, acc = 0;
             uint32_t phase = 0, uphase = 0, acc_phase = 0;
             for (;;) {
@@ -279,7 +304,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                 if (un.empty) continue;
                 const int a_mn = un.type == kUnitDW ? 1 : 0;
                 const int b_mn = un.type == kUnitGrad ? 0 : 1;
-                const uint32_t idesc = make_idesc_bf16(kBM, kBN, a_mn, b_mn);
+                const uint32_t idesc = make_idesc_bf16(kPM, kBN, a_mn, b_mn);
                 const int kbs = unit_kblocks(p, un);
                 mbar_wait(&tempty[acc], acc_phase ^ 1);
                 tc_fence_after();
@@ -287,40 +312,41 @@ __global__ void __launch_bounds__(kThreads, 1)
                 for (int kb = 0; kb < kbs; ++kb) {
                     mbar_wait(&full[stage], phase);
                     tc_fence_after();
-                    const uint32_t a_base = smem_u32(sA + stage * kStageBytesA);
-                    const uint32_t b_base = smem_u32(sB + stage * kStageBytesB);
+                    const uint32_t a_base = smem_u32(sA + stage * kPA);
+                    const uint32_t b_base = smem_u32(sB + stage * kPB);
 #pragma unroll
                     for (int k = 0; k < kBK / 16; ++k) {
                         const uint64_t ad = a_mn ? make_sdesc_sw128(a_base + k * 2048, 8192, 1024)
                                                  : make_sdesc_sw128(a_base + k * 32, 16, 1024);
                         const uint64_t bd = b_mn ? make_sdesc_sw128(b_base + k * 2048, 8192, 1024)
                                                  : make_sdesc_sw128(b_base + k * 32, 16, 1024);
-                        umma_bf16(d_tmem, ad, bd, idesc, (kb | k) != 0 ? 1u : 0u);
+                        umma_bf16_pair(d_tmem, ad, bd, idesc, (kb | k) != 0 ? 1u : 0u);
                     }
-                    umma_commit(&empty[stage]);
-                    if (++stage == kStages) {
+                    umma_commit_pair(&empty[stage], 0x3);
+                    if (++stage == kPS) {
                         stage = 0;
                         phase ^= 1;
                     }
                 }
-                umma_commit(&tfull[acc]);
+                umma_commit_pair(&tfull[acc], 0x3);
                 acc ^= 1;
                 if (acc == 0) acc_phase ^= 1;
             }
         }
     } else if (warp >= 4) {
-        // ------------------------------------------------ epilogue
+        // ------------------------------------------------ epilogue (both CTAs)
         const int q = warp & 3;
         const int r = q * 32 + lane;
         int us = 0, acc = 0;
         uint32_t uphase = 0, acc_phase = 0;
         const uint64_t pol_out = (p.l2_hints & 1) ? policy_evict_first() : policy_evict_normal();
         const uint64_t pol_gst = (p.l2_hints & 4) ? policy_evict_last() : policy_evict_normal();
+        const uint32_t leader_tempty0 = mapa_shared(&tempty[0], 0);
         for (;;) {
-            mbar_wait(&ufull[us], uphase);
+            mbar_wait_cluster(&ufull[us], uphase);
             const int u = unit_ring[us];
             __syncwarp();
-            if (lane == 0) mbar_arrive(&uempty[us]);
+            if (lane == 0) mbar_arrive_cluster(leader_uempty0 + 8 * us);
             if (++us == kUnitRing) {
                 us = 0;
                 uphase ^= 1;
@@ -333,8 +359,8 @@ __global__ void __launch_bounds__(kThreads, 1)
                 tc_fence_after();
                 const uint32_t taddr = tmem_base + (static_cast<uint32_t>(q * 32) << 16) +
                                        static_cast<uint32_t>(acc * kBN);
+                const int lrow = un.m_blk * kPM + static_cast<int>(rank) * 128 + r;
                 if (un.type == kUnitGrad) {
-                    const int lrow = un.m_blk * kBM + r;  // row inside the chunk
                     const bool row_ok = lrow < un.nc;
                     const int64_t grow = static_cast<int64_t>(un.r0) + lrow;
                     float gam = 0.f, l2lse = 0.f;
@@ -374,7 +400,6 @@ __global__ void __launch_bounds__(kThreads, 1)
                 } else {
                     // dH rows = chunk rows into dH; dW rows = band vocab rows into dW
                     const bool is_dh = un.type == kUnitDH;
-                    const int lrow = un.m_blk * kBM + r;
                     const int mrows = is_dh ? un.nc : un.vc;
                     const bool accumulate = is_dh ? (un.band_idx > 0 || p.accumulate_dh) : (un.row_idx > 0);
                     float* crow = is_dh ? p.dh + (static_cast<int64_t>(un.r0) + lrow) * p.lddh
@@ -412,15 +437,15 @@ __global__ void __launch_bounds__(kThreads, 1)
                 }
                 tc_fence_before();
                 __syncwarp();
-                if (lane == 0) mbar_arrive(&tempty[acc]);
+                if (lane == 0) mbar_arrive_cluster(leader_tempty0 + 8 * acc);
                 acc ^= 1;
                 if (acc == 0) acc_phase ^= 1;
                 // generic-proxy stores above are read later through TMA (async proxy)
                 fence_proxy_async_global();
             }
 
-            // publish completion: all 128 epilogue threads' stores, then one
-            // gpu-scope release
+            // publish completion of this CTA's half: all 128 epilogue threads'
+            // stores, then one gpu-scope release
             named_bar_sync(1, 128);
             if (threadIdx.x == 128) {
                 __threadfence();
@@ -439,24 +464,26 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
 
     tc_fence_before();
-    __syncthreads();
+    cluster_sync_all();
     tc_fence_after();
-    if (warp == 2) tmem_dealloc<512>(tmem_base);
+    if (warp == 2) tmem_dealloc_pair<512>(tmem_base);
 }
+
+constexpr int kBwdSmem = kPS * (kPA + kPB) + 1024 + 512;
 
 cudaError_t launch_bwd_persistent(const BwdParams& p, const BwdMaps& maps, int grid,
                                   cudaStream_t stream) {
     static bool attr_done = false;
-    const int smem = kSmemBytes + 256;
     if (!attr_done) {
         cudaError_t e = cudaFuncSetAttribute(fce_bwd_persistent_kernel,
-                                             cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+                                             cudaFuncAttributeMaxDynamicSharedMemorySize, kBwdSmem);
         if (e != cudaSuccess) return e;
         attr_done = true;
     }
-    if (grid > p.units) grid = p.units;
-    if (grid < 1) return cudaSuccess;
-    fce_bwd_persistent_kernel<<<grid, kThreads, smem, stream>>>(p, maps);
+    int pairs = grid / 2;
+    if (pairs > p.units) pairs = p.units;
+    if (pairs < 1) return cudaSuccess;
+    fce_bwd_persistent_kernel<<<2 * pairs, kThreads, kBwdSmem, stream>>>(p, maps);
     return cudaGetLastError();
 }
 

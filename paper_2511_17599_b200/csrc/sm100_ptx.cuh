@@ -314,3 +314,21 @@ __device__ __forceinline__ void umma_commit_pair(uint64_t* bar, uint16_t mask) {
 
 }  // namespace ptx
 }  // namespace fce
+
+namespace fce {
+namespace ptx {
+// try_wait with cluster-scope acquire: for barriers a peer CTA arrives on
+// after writing this CTA's shared memory remotely.
+__device__ __forceinline__ void mbar_wait_cluster(uint64_t* bar, uint32_t parity) {
+    asm volatile(
+        "{\n"
+        ".reg .pred P1;\n"
+        "WAITC_%=:\n"
+        "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 P1, [%0], %1;\n"
+        "@!P1 bra WAITC_%=;\n"
+        "}\n" ::"r"(smem_u32(bar)),
+        "r"(parity)
+        : "memory");
+}
+}  // namespace ptx
+}  // namespace fce
