@@ -55,6 +55,7 @@ struct fce_handle_s {
     int64_t splits = 0, band_cols = 0, row_chunk = 0, validate = 1, bwd_persistent = 1;
     int64_t l2_hints = 1;
     int64_t gemm_pair = 1;
+    int64_t bwd_unit_mask = 7;
     int64_t launches = 0;
     size_t bwd_scratch[4] = {0, 0, 0, 0};  // offsets of the persistent-backward scratch
     // optional per-kernel CUDA-event timing of the tile kernels (bench roofline)
@@ -301,6 +302,7 @@ fce_status run_backward_persistent(fce_handle h, const fce_problem* p, const flo
     bp.has_ignore = p->has_ignore;
     bp.accumulate_dh = accumulate_dhidden;
     bp.l2_hints = static_cast<int>(h->l2_hints);
+    bp.unit_mask = static_cast<int>(h->bwd_unit_mask);
     bp.nc_max = row_chunk;
     bp.ldg = band;
     bp.d = p->d;
@@ -444,6 +446,8 @@ fce_status fce_set_option(fce_handle h, const char* key, int64_t value) {
         h->row_chunk = value;
     } else if (!std::strcmp(key, "validate")) {
         h->validate = value ? 1 : 0;
+    } else if (!std::strcmp(key, "bwd_unit_mask")) {
+        h->bwd_unit_mask = value & 7;
     } else if (!std::strcmp(key, "gemm_pair")) {
         h->gemm_pair = value ? 1 : 0;
     } else if (!std::strcmp(key, "l2_hints")) {

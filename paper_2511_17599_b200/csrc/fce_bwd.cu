@@ -95,6 +95,7 @@ __device__ __forceinline__ BUnit decode_unit(const BwdParams& p, int u) {
         r.m_blk = l2 - r.n_tile * p.vm;
         r.empty = r.m_blk * kPM >= r.vc;
     }
+    if (!((p.unit_mask >> r.type) & 1)) r.empty = true;
     return r;
 }
 
