@@ -447,7 +447,7 @@ fce_status fce_set_option(fce_handle h, const char* key, int64_t value) {
     } else if (!std::strcmp(key, "validate")) {
         h->validate = value ? 1 : 0;
     } else if (!std::strcmp(key, "bwd_unit_mask")) {
-        h->bwd_unit_mask = value & 7;
+        h->bwd_unit_mask = value & 31;
     } else if (!std::strcmp(key, "gemm_pair")) {
         h->gemm_pair = value ? 1 : 0;
     } else if (!std::strcmp(key, "l2_hints")) {

@@ -195,7 +195,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
             const uint32_t leader_full0 = mapa_shared(&full[0], 0);
             const uint32_t peer_ring0 = mapa_shared(&unit_ring[0], 1);
             const uint32_t peer_ufull0 = mapa_shared(&ufull[0], 1);
-            int u_next = rank == 0 ? static_cast<int>(atomicAdd(p.counters, 1u)) : 0;
+            // debug bit 4 of unit_mask: static round-robin schedule instead of work stealing
+            const bool static_sched = (p.unit_mask >> 4) & 1;
+            int u_static = blockIdx.x >> 1;
+            int u_next = rank == 0 ? (static_sched ? u_static : static_cast<int>(atomicAdd(p.counters, 1u))) : 0;
             for (;;) {
                 int u;
                 if (rank == 0) {
@@ -219,7 +222,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
                 if (un.type == kUnitStop) break;
                 // claim the next unit now; the atomic's latency hides behind this
                 // unit's loads (its result is first used at the top of the loop)
-                if (rank == 0) u_next = static_cast<int>(atomicAdd(p.counters, 1u));
+                if (rank == 0) {
+                    u_static += gridDim.x >> 1;
+                    u_next = static_sched ? u_static : static_cast<int>(atomicAdd(p.counters, 1u));
+                }
                 if (un.empty) continue;
                 const CUtensorMap *ma, *mb;
                 int a_mn, b_mn, a_row, b_row, a_k0, b_k0;
@@ -380,7 +386,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
                         float v[32];
                         tmem_ld32(taddr + c * 32, v);
                         const int col0 = un.n_tile * kBN + c * 32;
-                        if (row_ok) {
+                        if (row_ok && !((p.unit_mask >> 3) & 1)) {  // debug bit 3: skip G stores
                             const int64_t tc = tcol - col0;
                             uint32_t packed[16];
 #pragma unroll
