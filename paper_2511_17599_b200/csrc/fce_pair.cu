@@ -41,6 +41,16 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     const int m_tiles = (q.m + 255) / 256;
     const int n_tiles = (q.n + 255) / 256;
     const int units = m_tiles * n_tiles;
+    // L2 raster: groups of kGroupM row tiles, row tile fastest inside a group
+    constexpr int kGroupM = 8;
+    auto tile_of = [&](int u, int& mt, int& nt) {
+        const int per_group = kGroupM * n_tiles;
+        const int g = u / per_group;
+        const int gsize = min(kGroupM, m_tiles - g * kGroupM);
+        const int l = u - g * per_group;
+        nt = l / gsize;
+        mt = g * kGroupM + (l - nt * gsize);
+    };
 
     if (threadIdx.x == 0) {
         for (int s = 0; s < kPairStages; ++s) {
@@ -69,7 +79,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
             int stage = 0;
             uint32_t phase = 0;
             for (int u = pair; u < units; u += n_pairs) {
-                const int nt = u / m_tiles, mt = u - nt * m_tiles;
+                int mt, nt;
+                tile_of(u, mt, nt);
                 const int a_row = mt * 256 + rank * 128;
                 const int b_row = nt * 256 + rank * 128;
                 for (int kb = 0; kb < q.k_blocks; ++kb) {
@@ -142,7 +153,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         int acc = 0;
         uint32_t acc_phase = 0;
         for (int u = pair; u < units; u += n_pairs) {
-            const int nt = u / m_tiles, mt = u - nt * m_tiles;
+            int mt, nt;
+            tile_of(u, mt, nt);
             const int64_t row = static_cast<int64_t>(mt) * 256 + rank * 128 + r;
             mbar_wait(&tfull[acc], acc_phase);
             tc_fence_after();
