@@ -99,6 +99,12 @@ __device__ __forceinline__ BUnit decode_unit(const BwdParams& p, int u) {
     return r;
 }
 
+__device__ __forceinline__ unsigned long long global_ns() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+
 __device__ __forceinline__ unsigned ld_acquire(const unsigned* ptr) {
     unsigned v;
     asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(ptr) : "memory");
@@ -313,6 +319,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
                 const int b_mn = un.type == kUnitGrad ? 0 : 1;
                 const uint32_t idesc = make_idesc_bf16(kPM, kBN, a_mn, b_mn);
                 const int kbs = unit_kblocks(p, un);
+                if (p.trace) p.trace[4 * u + 0] = global_ns();
                 mbar_wait(&tempty[acc], acc_phase ^ 1);
                 tc_fence_after();
                 const uint32_t d_tmem = tmem_base + acc * kBN;
@@ -336,6 +343,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
                     }
                 }
                 umma_commit_pair(&tfull[acc], 0x3);
+                if (p.trace) p.trace[4 * u + 1] = global_ns();
                 acc ^= 1;
                 if (acc == 0) acc_phase ^= 1;
             }
@@ -456,6 +464,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
             named_bar_sync(1, 128);
             if (threadIdx.x == 128) {
                 __threadfence();
+                if (p.trace && rank == 0) {
+                    unsigned smid;
+                    asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+                    p.trace[4 * u + 2] = global_ns();
+                    p.trace[4 * u + 3] = smid;
+                }
                 if (un.type == kUnitGrad) {
                     atomicAdd(p.counters + p.gm_base + un.c * p.mb_max + un.m_blk, 1u);
                     atomicAdd(cnt(p, un.c, 0), 1u);
