@@ -15,7 +15,16 @@ LIB       := $(PKG)/libfce.so
 ORACLE    := oracle/liboracle.so
 REF_LIB   := oracle/_ref/libfce_ref.so
 
-all: $(LIB) $(ORACLE) ref
+DROPIN_TEST := tests/cpp/test_dropin
+
+all: $(LIB) $(ORACLE) ref $(DROPIN_TEST)
+
+# C++ drop-in API (include/fusedce) against the oracle; runs on a B200
+$(DROPIN_TEST): tests/cpp/test_dropin.cpp $(wildcard include/fusedce/*.hpp include/fusedce/detail/*.hpp) \
+                include/fce/fce.h $(LIB) $(ORACLE)
+	$(CXX) -std=c++20 -O2 -Iinclude -I/usr/local/cuda/include -o $@ tests/cpp/test_dropin.cpp \
+	    -L$(PKG) -lfce -Loracle -loracle -L/usr/local/cuda/lib64 -lcudart \
+	    -Wl,-rpath,'$$ORIGIN/../../$(PKG)' -Wl,-rpath,'$$ORIGIN/../../oracle' -Wl,-rpath,/usr/local/cuda/lib64
 
 $(LIB): $(CSRC)/fce_kernels.cu $(CSRC)/fce_bwd.cu $(CSRC)/fce_pair.cu $(CSRC)/fce_api.cpp $(CSRC)/fce_vp.cpp $(CSRC)/fce_internal.h \
         $(CSRC)/sm100_ptx.cuh include/fce/fce.h
@@ -37,6 +46,6 @@ $(REF_LIB): oracle/ref_shim.cpp
 	    -I$(REF_DIR)/include -o $@ oracle/ref_shim.cpp
 
 clean:
-	rm -f $(LIB) $(ORACLE) $(REF_LIB)
+	rm -f $(LIB) $(ORACLE) $(REF_LIB) $(DROPIN_TEST)
 
 .PHONY: all ref clean
