@@ -451,7 +451,7 @@ fce_status fce_set_option(fce_handle h, const char* key, int64_t value) {
     } else if (!std::strcmp(key, "trace_ptr")) {
         h->trace_ptr = value;
     } else if (!std::strcmp(key, "bwd_unit_mask")) {
-        h->bwd_unit_mask = value & 31;
+        h->bwd_unit_mask = value & 63;
     } else if (!std::strcmp(key, "gemm_pair")) {
         h->gemm_pair = value ? 1 : 0;
     } else if (!std::strcmp(key, "l2_hints")) {

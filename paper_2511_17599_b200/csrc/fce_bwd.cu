@@ -424,7 +424,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
                         float v[32];
                         tmem_ld32(taddr + c * 32, v);
                         const int col0 = un.n_tile * kBN + c * 32;
-                        if (lrow < mrows) {
+                        if (lrow < mrows && !((p.unit_mask >> 5) & 1)) {  // debug bit 5: discard dH/dW
                             float* dst = crow + col0;
                             const bool vec = (col0 + 32 <= p.d) && ((reinterpret_cast<uintptr_t>(dst) & 15) == 0);
                             if (vec) {
