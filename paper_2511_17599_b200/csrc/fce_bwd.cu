@@ -41,7 +41,7 @@ namespace fce {
 using namespace ptx;
 
 static constexpr float kL2e = 1.4426950408889634f;
-constexpr int kUnitRing = 4;
+constexpr int kUnitRing = 8;
 constexpr int kPS = 6;                     // pipeline stages
 constexpr int kPA = 128 * kBK * 2;         // this CTA's A rows per stage
 constexpr int kPB = 128 * kBK * 2;         // this CTA's B columns per stage
@@ -170,8 +170,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         }
         for (int s = 0; s < kUnitRing; ++s) {
             mbar_init(&ufull[s], 1);
-            // leader's copy: MMA thread + 4 epilogue warps of each CTA + peer producer
-            mbar_init(&uempty[s], 10);
+            // leader's copy: TMA producer + 4 epilogue warps of each CTA, + MMA thread
+            mbar_init(&uempty[s], 11);
         }
         fence_mbar_init();
     }
@@ -190,8 +190,52 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     const uint32_t tmem_base = *tmem_slot;
     const uint32_t leader_uempty0 = mapa_shared(&uempty[0], 0);
 
-    if (warp == 0) {
-        // ------------------------------------------------ scheduler + TMA producer
+    if (warp == 3) {
+        // ------------------------------------------------ scheduler (even CTA)
+        // Claims units (work stealing per pair), waits until their inputs are
+        // complete, and only then publishes them to both CTAs' unit rings, so
+        // dependency latency never sits on the TMA / MMA critical path.
+        if (lane == 0 && rank == 0) {
+            int us = 0;
+            uint32_t uphase = 0;
+            const uint32_t peer_ring0 = mapa_shared(&unit_ring[0], 1);
+            const uint32_t peer_ufull0 = mapa_shared(&ufull[0], 1);
+            const bool static_sched = (p.unit_mask >> 4) & 1;  // debug: round-robin schedule
+            int u_static = blockIdx.x >> 1;
+            for (;;) {
+                int u;
+                if (static_sched) {
+                    u = u_static;
+                    u_static += gridDim.x >> 1;
+                } else {
+                    u = static_cast<int>(atomicAdd(p.counters, 1u));
+                }
+                const BUnit un = decode_unit(p, u);
+                if (un.type != kUnitStop && !un.empty) {
+                    if (un.type == kUnitGrad) {
+                        if (un.c >= 2) wait_at_least(cnt(p, un.c - 2, 3), two * (p.n_dh + p.n_dw));
+                    } else if (un.type == kUnitDH) {
+                        wait_at_least(p.counters + p.gm_base + un.c * p.mb_max + un.m_blk, two * p.vt);
+                        if (un.band_idx > 0) wait_at_least(cnt(p, un.c - 1, 1), two * p.n_dh);
+                    } else {
+                        wait_at_least(cnt(p, un.c, 0), two * p.n_g);
+                        if (un.row_idx > 0) wait_at_least(cnt(p, un.c - p.bands, 2), two * p.n_dw);
+                    }
+                }
+                mbar_wait_cluster(&uempty[us], uphase ^ 1);
+                unit_ring[us] = u;
+                st_shared_cluster_u32(peer_ring0 + 4 * us, static_cast<uint32_t>(u));
+                mbar_arrive(&ufull[us]);
+                mbar_arrive_cluster(peer_ufull0 + 8 * us);
+                if (++us == kUnitRing) {
+                    us = 0;
+                    uphase ^= 1;
+                }
+                if (un.type == kUnitStop) break;
+            }
+        }
+    } else if (warp == 0) {
+        // ------------------------------------------------ TMA producer (both CTAs)
         if (lane == 0) {
             int stage = 0, us = 0;
             uint32_t phase = 0, uphase = 0;
@@ -199,45 +243,21 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
             const uint64_t pol_g = (p.l2_hints & 2) ? policy_evict_last() : pol_norm;
             const uint64_t pol_h = (p.l2_hints & 8) ? policy_evict_first() : pol_norm;
             const uint32_t leader_full0 = mapa_shared(&full[0], 0);
-            const uint32_t peer_ring0 = mapa_shared(&unit_ring[0], 1);
-            const uint32_t peer_ufull0 = mapa_shared(&ufull[0], 1);
-            // debug bit 4 of unit_mask: static round-robin schedule instead of work stealing
-            const bool static_sched = (p.unit_mask >> 4) & 1;
-            int u_static = blockIdx.x >> 1;
-            int u_next = rank == 0 ? (static_sched ? u_static : static_cast<int>(atomicAdd(p.counters, 1u))) : 0;
             for (;;) {
-                int u;
-                if (rank == 0) {
-                    // publish the unit to both CTAs of the pair
-                    u = u_next;
-                    mbar_wait_cluster(&uempty[us], uphase ^ 1);
-                    unit_ring[us] = u;
-                    st_shared_cluster_u32(peer_ring0 + 4 * us, static_cast<uint32_t>(u));
-                    mbar_arrive(&ufull[us]);
-                    mbar_arrive_cluster(peer_ufull0 + 8 * us);
-                } else {
-                    mbar_wait_cluster(&ufull[us], uphase);
-                    u = unit_ring[us];
-                    mbar_arrive_cluster(leader_uempty0 + 8 * us);
-                }
+                mbar_wait_cluster(&ufull[us], uphase);
+                const int u = unit_ring[us];
+                mbar_arrive_cluster(leader_uempty0 + 8 * us);
                 if (++us == kUnitRing) {
                     us = 0;
                     uphase ^= 1;
                 }
                 const BUnit un = decode_unit(p, u);
                 if (un.type == kUnitStop) break;
-                // claim the next unit now; the atomic's latency hides behind this
-                // unit's loads (its result is first used at the top of the loop)
-                if (rank == 0) {
-                    u_static += gridDim.x >> 1;
-                    u_next = static_sched ? u_static : static_cast<int>(atomicAdd(p.counters, 1u));
-                }
                 if (un.empty) continue;
                 const CUtensorMap *ma, *mb;
                 int a_mn, b_mn, a_row, b_row, a_k0, b_k0;
                 uint64_t pa = pol_norm, pb = pol_norm;
                 if (un.type == kUnitGrad) {
-                    if (un.c >= 2) wait_at_least(cnt(p, un.c - 2, 3), two * (p.n_dh + p.n_dw));
                     ma = &maps.h_k;
                     mb = &maps.w_k;
                     a_mn = b_mn = 0;
@@ -245,8 +265,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
                     b_row = un.vb + un.n_tile * kBN + rank * 128;
                     a_k0 = b_k0 = 0;
                 } else if (un.type == kUnitDH) {
-                    wait_at_least(p.counters + p.gm_base + un.c * p.mb_max + un.m_blk, two * p.vt);
-                    if (un.band_idx > 0) wait_at_least(cnt(p, un.c - 1, 1), two * p.n_dh);
                     ma = &maps.g_k;
                     mb = &maps.w_mn;
                     a_mn = 0;
@@ -257,8 +275,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
                     b_k0 = un.vb;
                     pa = pol_g;
                 } else {
-                    wait_at_least(cnt(p, un.c, 0), two * p.n_g);
-                    if (un.row_idx > 0) wait_at_least(cnt(p, un.c - p.bands, 2), two * p.n_dw);
                     ma = &maps.g_mn;
                     mb = &maps.h_mn;
                     a_mn = b_mn = 1;
@@ -269,7 +285,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
                     pa = pol_g;
                     pb = pol_h;
                 }
-                // order the acquires above before this thread's async-proxy (TMA) reads
+                // the scheduler acquired this unit's inputs (gpu scope) before
+                // publishing it; order that before this thread's async-proxy reads
                 fence_proxy_async_global();
                 const int kbs = unit_kblocks(p, un);
                 for (int kb = 0; kb < kbs; ++kb) {
