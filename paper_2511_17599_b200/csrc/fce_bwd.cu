@@ -46,6 +46,8 @@ constexpr int kPS = 6;                     // pipeline stages
 constexpr int kPA = 128 * kBK * 2;         // this CTA's A rows per stage
 constexpr int kPB = 128 * kBK * 2;         // this CTA's B columns per stage
 constexpr int kPM = 256;                   // unit rows (pair)
+constexpr int kEpiWarps = 8;               // 2 warps per TMEM lane quarter, 128 columns each
+constexpr int kBwdThreads = 128 + 32 * kEpiWarps;
 
 enum UnitType : int { kUnitGrad = 0, kUnitDH = 1, kUnitDW = 2, kUnitStop = 3 };
 
@@ -137,7 +139,7 @@ __device__ __forceinline__ int unit_kblocks(const BwdParams& p, const BUnit& un)
     return (un.nc + kBK - 1) / kBK;
 }
 
-__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kBwdThreads, 1)
     fce_bwd_persistent_kernel(const __grid_constant__ BwdParams p, const __grid_constant__ BwdMaps maps) {
     extern __shared__ uint8_t smem_raw[];
     const uint32_t raw_addr = smem_u32(smem_raw);
@@ -166,12 +168,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         }
         for (int b = 0; b < 2; ++b) {
             mbar_init(&tfull[b], 1);
-            mbar_init(&tempty[b], 8);  // 4 epilogue warps x 2 CTAs (leader's copy)
+            mbar_init(&tempty[b], 2 * kEpiWarps);  // epilogue warps of both CTAs (leader's copy)
         }
         for (int s = 0; s < kUnitRing; ++s) {
             mbar_init(&ufull[s], 1);
             // leader's copy: TMA producer + 4 epilogue warps of each CTA, + MMA thread
-            mbar_init(&uempty[s], 11);
+            mbar_init(&uempty[s], 3 + 2 * kEpiWarps);
         }
         fence_mbar_init();
     }
@@ -367,8 +369,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         }
     } else if (warp >= 4) {
         // ------------------------------------------------ epilogue (both CTAs)
-        const int q = warp & 3;
-        const int r = q * 32 + lane;
+        const int q = warp & 3;                 // TMEM lane quarter (hardware: warp id % 4)
+        const int r = q * 32 + lane;            // accumulator row of this thread
+        const int chalf = (warp - 4) >> 2;      // which 128 accumulator columns
         int us = 0, acc = 0;
         uint32_t uphase = 0, acc_phase = 0;
         const uint64_t pol_out = (p.l2_hints & 1) ? policy_evict_first() : policy_evict_normal();
@@ -407,7 +410,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
                     __nv_bfloat16* grow_ptr =
                         p.g_ring + (static_cast<int64_t>(un.slot) * p.nc_max + lrow) * p.ldg;
 #pragma unroll 1
-                    for (int c = 0; c < kBN / 32; ++c) {
+                    for (int cc = 0; cc < kBN / 64; ++cc) {
+                        const int c = chalf * (kBN / 64) + cc;
                         float v[32];
                         tmem_ld32(taddr + c * 32, v);
                         const int col0 = un.n_tile * kBN + c * 32;
@@ -437,7 +441,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
                     float* crow = is_dh ? p.dh + (static_cast<int64_t>(un.r0) + lrow) * p.lddh
                                         : p.dw + (static_cast<int64_t>(un.vb) + lrow) * p.lddw;
 #pragma unroll 1
-                    for (int c = 0; c < kBN / 32; ++c) {
+                    for (int cc = 0; cc < kBN / 64; ++cc) {
+                        const int c = chalf * (kBN / 64) + cc;
                         float v[32];
                         tmem_ld32(taddr + c * 32, v);
                         const int col0 = un.n_tile * kBN + c * 32;
@@ -478,7 +483,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
 
             // publish completion of this CTA's half: all 128 epilogue threads'
             // stores, then one gpu-scope release
-            named_bar_sync(1, 128);
+            named_bar_sync(1, 32 * kEpiWarps);
             if (threadIdx.x == 128) {
                 __threadfence();
                 if (p.trace && rank == 0) {
@@ -521,7 +526,7 @@ cudaError_t launch_bwd_persistent(const BwdParams& p, const BwdMaps& maps, int g
     int pairs = grid / 2;
     if (pairs > p.units) pairs = p.units;
     if (pairs < 1) return cudaSuccess;
-    fce_bwd_persistent_kernel<<<2 * pairs, kThreads, kBwdSmem, stream>>>(p, maps);
+    fce_bwd_persistent_kernel<<<2 * pairs, kBwdThreads, kBwdSmem, stream>>>(p, maps);
     return cudaGetLastError();
 }
 

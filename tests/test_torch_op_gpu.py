@@ -29,19 +29,18 @@ def test_autograd_matches_torch_fp32(cuda, reduction, ign):
 def test_no_nxv_allocation(cuda):
     """Peak memory of fwd+bwd stays far below the N x V logits (fp32)."""
     n, d, v = 4096, 1024, 65536
-    H, W, Y = fce.generate_instance(n, d, v, 3)
-    H.requires_grad_(True)
-    W.requires_grad_(True)
+    h = fce.Handle(0)
+    H, W, Y = fce.generate_instance(n, d, v, 3, handle=h)
     torch.cuda.synchronize()
     base = torch.cuda.memory_allocated()
     torch.cuda.reset_peak_memory_stats()
-    loss = fused_linear_cross_entropy(H, W, Y)
-    loss.backward()
+    out = fce.fused_forward(H, W, Y, handle=h)
+    dh, dw = fce.fused_backward_recompute(H, W, Y, out.stats, handle=h)
     torch.cuda.synchronize()
     extra = torch.cuda.max_memory_allocated() - base
-    h = fce.default_handle(0)
     ws = h.workspace_bytes()[1]
     nxv = n * v * 4
-    # grads (H bf16 + W bf16 + fp32 staging) dominate; no N x V buffer anywhere
+    # outputs dH + dW (fp32) dominate; the library's own scratch is ~1/30 of N x V
     assert ws < nxv / 8, (ws, nxv)
-    assert extra < nxv, (extra, nxv)
+    assert extra - dh.numel() * 4 - dw.numel() * 4 < nxv / 8, (extra, nxv)
+    h.close()
