@@ -56,7 +56,8 @@ struct fce_handle_s {
     int64_t l2_hints = 1;
     int64_t gemm_pair = 1;
     int64_t bwd_unit_mask = 7;
-    int64_t trace_ptr = 0;  // dev only: device buffer for per-unit timestamps
+    int64_t trace_ptr = 0;
+    int64_t bwd_epi_warps = 8;  // dev only: device buffer for per-unit timestamps
     int64_t launches = 0;
     size_t bwd_scratch[4] = {0, 0, 0, 0};  // offsets of the persistent-backward scratch
     // optional per-kernel CUDA-event timing of the tile kernels (bench roofline)
@@ -304,6 +305,7 @@ fce_status run_backward_persistent(fce_handle h, const fce_problem* p, const flo
     bp.accumulate_dh = accumulate_dhidden;
     bp.l2_hints = static_cast<int>(h->l2_hints);
     bp.unit_mask = static_cast<int>(h->bwd_unit_mask);
+    bp.epi_warps = static_cast<int>(h->bwd_epi_warps);
     bp.trace = reinterpret_cast<unsigned long long*>(h->trace_ptr);
     bp.nc_max = row_chunk;
     bp.ldg = band;
@@ -448,6 +450,9 @@ fce_status fce_set_option(fce_handle h, const char* key, int64_t value) {
         h->row_chunk = value;
     } else if (!std::strcmp(key, "validate")) {
         h->validate = value ? 1 : 0;
+    } else if (!std::strcmp(key, "bwd_epi_warps")) {
+        if (value != 4 && value != 8) return fail(FCE_INVALID_ARGUMENT, "bwd_epi_warps must be 4 or 8");
+        h->bwd_epi_warps = value;
     } else if (!std::strcmp(key, "trace_ptr")) {
         h->trace_ptr = value;
     } else if (!std::strcmp(key, "bwd_unit_mask")) {

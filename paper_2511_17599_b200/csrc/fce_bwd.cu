@@ -46,8 +46,8 @@ constexpr int kPS = 6;                     // pipeline stages
 constexpr int kPA = 128 * kBK * 2;         // this CTA's A rows per stage
 constexpr int kPB = 128 * kBK * 2;         // this CTA's B columns per stage
 constexpr int kPM = 256;                   // unit rows (pair)
-constexpr int kEpiWarps = 8;               // 2 warps per TMEM lane quarter, 128 columns each
-constexpr int kBwdThreads = 128 + 32 * kEpiWarps;
+// epilogue warps: 4 (one per TMEM lane quarter, 256 columns each) or 8 (two per
+// quarter, 128 columns each); selected at launch (option "bwd_epi_warps")
 
 enum UnitType : int { kUnitGrad = 0, kUnitDH = 1, kUnitDW = 2, kUnitStop = 3 };
 
@@ -139,7 +139,8 @@ __device__ __forceinline__ int unit_kblocks(const BwdParams& p, const BUnit& un)
     return (un.nc + kBK - 1) / kBK;
 }
 
-__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kBwdThreads, 1)
+template <int kEpiWarps>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(128 + 32 * kEpiWarps, 1)
     fce_bwd_persistent_kernel(const __grid_constant__ BwdParams p, const __grid_constant__ BwdMaps maps) {
     extern __shared__ uint8_t smem_raw[];
     const uint32_t raw_addr = smem_u32(smem_raw);
@@ -371,7 +372,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kBwdThreads, 1)
         // ------------------------------------------------ epilogue (both CTAs)
         const int q = warp & 3;                 // TMEM lane quarter (hardware: warp id % 4)
         const int r = q * 32 + lane;            // accumulator row of this thread
-        const int chalf = (warp - 4) >> 2;      // which 128 accumulator columns
+        const int chalf = (warp - 4) >> 2;      // which column slice (8 warps: halves)
         int us = 0, acc = 0;
         uint32_t uphase = 0, acc_phase = 0;
         const uint64_t pol_out = (p.l2_hints & 1) ? policy_evict_first() : policy_evict_normal();
@@ -410,8 +411,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kBwdThreads, 1)
                     __nv_bfloat16* grow_ptr =
                         p.g_ring + (static_cast<int64_t>(un.slot) * p.nc_max + lrow) * p.ldg;
 #pragma unroll 1
-                    for (int cc = 0; cc < kBN / 64; ++cc) {
-                        const int c = chalf * (kBN / 64) + cc;
+                    for (int cc = 0; cc < kBN / 32 / (kEpiWarps / 4); ++cc) {
+                        const int c = chalf * (kBN / 32 / (kEpiWarps / 4)) + cc;
                         float v[32];
                         tmem_ld32(taddr + c * 32, v);
                         const int col0 = un.n_tile * kBN + c * 32;
@@ -441,8 +442,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kBwdThreads, 1)
                     float* crow = is_dh ? p.dh + (static_cast<int64_t>(un.r0) + lrow) * p.lddh
                                         : p.dw + (static_cast<int64_t>(un.vb) + lrow) * p.lddw;
 #pragma unroll 1
-                    for (int cc = 0; cc < kBN / 64; ++cc) {
-                        const int c = chalf * (kBN / 64) + cc;
+                    for (int cc = 0; cc < kBN / 32 / (kEpiWarps / 4); ++cc) {
+                        const int c = chalf * (kBN / 32 / (kEpiWarps / 4)) + cc;
                         float v[32];
                         tmem_ld32(taddr + c * 32, v);
                         const int col0 = un.n_tile * kBN + c * 32;
@@ -516,17 +517,18 @@ constexpr int kBwdSmem = kPS * (kPA + kPB) + 1024 + 512;
 
 cudaError_t launch_bwd_persistent(const BwdParams& p, const BwdMaps& maps, int grid,
                                   cudaStream_t stream) {
-    static bool attr_done = false;
-    if (!attr_done) {
-        cudaError_t e = cudaFuncSetAttribute(fce_bwd_persistent_kernel,
-                                             cudaFuncAttributeMaxDynamicSharedMemorySize, kBwdSmem);
+    static bool attr_done[2] = {false, false};
+    const int wide = p.epi_warps == 4 ? 0 : 1;
+    auto kern = wide ? fce_bwd_persistent_kernel<8> : fce_bwd_persistent_kernel<4>;
+    if (!attr_done[wide]) {
+        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, kBwdSmem);
         if (e != cudaSuccess) return e;
-        attr_done = true;
+        attr_done[wide] = true;
     }
     int pairs = grid / 2;
     if (pairs > p.units) pairs = p.units;
     if (pairs < 1) return cudaSuccess;
-    fce_bwd_persistent_kernel<<<2 * pairs, kBwdThreads, kBwdSmem, stream>>>(p, maps);
+    kern<<<2 * pairs, 128 + 32 * (wide ? 8 : 4), kBwdSmem, stream>>>(p, maps);
     return cudaGetLastError();
 }
 

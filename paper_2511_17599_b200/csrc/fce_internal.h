@@ -78,6 +78,7 @@ struct BwdParams {
     int n, v;                // rows, local vocab rows
     int has_ignore, accumulate_dh;
     int unit_mask;           // debug / profiling: bit0 grad, bit1 dH, bit2 dW units do work
+    int epi_warps;           // 4 or 8 epilogue warps per CTA
     int l2_hints;            // bit0: evict_first on dH/dW writes, bit1: evict_last on G loads,
                              // bit2: evict_last on G stores, bit3: evict_first on H loads (dW)
     int64_t nc_max, ldg, d, lddh, lddw, v_offset, ignore_index;
