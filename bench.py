@@ -145,7 +145,7 @@ def cpu_sample_inputs(n_rows, d, v, frac):
 def cpu_baseline(cfg_name, budget_s=20.0):
     """Reference CPU path on this host: rows sample sized to ~budget_s of work."""
     n, d, v, frac = CONFIGS[cfg_name]
-    rows = min(n, 4)
+    rows = min(n, os.cpu_count() or 1, 16)  # one row per host core: every core busy
     H, W, Y = cpu_sample_inputs(64 if n >= 64 else n, d, v, frac)
     dt, kind, cores, fw, bw = cpu_reference_step(rows, d, v, frac, H[:rows], W, Y[:rows])
     if dt < budget_s / 4 and rows < n:
@@ -162,7 +162,7 @@ def run_reference_arm(args):
     if rank != 0:
         return 0
     n, d, v, frac = CONFIGS[args.config]
-    rows = args.ref_rows
+    rows = min(n, args.ref_rows or min(os.cpu_count() or 1, 16))
     H, W, Y = cpu_sample_inputs(max(rows, 1), d, v, frac)
     for _ in range(args.warmup if args.ref_warmup else 0):
         cpu_reference_step(rows, d, v, frac, H[:rows], W, Y[:rows])
@@ -196,7 +196,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--config", default="llama3-8b", choices=sorted(CONFIGS))
     ap.add_argument("--impl", default="fce", choices=["fce", "reference"])
-    ap.add_argument("--ref-rows", type=int, default=2)
+    ap.add_argument("--ref-rows", type=int, default=0, help="rows per reference step (0: one per host core, <= 16)")
     ap.add_argument("--ref-warmup", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=3)
