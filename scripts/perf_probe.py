@@ -4,16 +4,18 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import paper_2511_17599_b200 as fce
 n, d, v = (int(x) for x in (sys.argv[1:4] if len(sys.argv) > 3 else (16384, 4096, 128256)))
 opts = dict(a.split("=") for a in sys.argv[4:])
-H, W, Y = fce.generate_instance(n, d, v, 42)
+frac = float(opts.pop("ignore_fraction", 0.0))
+H, W, Y = fce.generate_instance(n, d, v, 42, -100, frac)
+ign = -100 if frac > 0 else None
 h = fce.default_handle(0)
 for k, val in opts.items():
     h.set_option(k, int(val))
 h.set_option("validate", 0)
 def fwd():
-    return fce.fused_forward(H, W, Y, "mean", handle=h)
+    return fce.fused_forward(H, W, Y, "mean", ign, handle=h)
 out = fwd()
 def bwd():
-    return fce.fused_backward_recompute(H, W, Y, out.stats, "mean", 1.0, handle=h)
+    return fce.fused_backward_recompute(H, W, Y, out.stats, "mean", 1.0, ign, handle=h)
 for f in (fwd, bwd): f()
 torch.cuda.synchronize()
 def t(f, it=3):
