@@ -339,12 +339,24 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(128 + 32 * kEpiWarps
                 const int b_mn = un.type == kUnitGrad ? 0 : 1;
                 const uint32_t idesc = make_idesc_bf16(kPM, kBN, a_mn, b_mn);
                 const int kbs = unit_kblocks(p, un);
-                if (p.trace) p.trace[4 * u + 0] = global_ns();
+                if (p.trace) p.trace[8 * u + 0] = global_ns();
                 mbar_wait(&tempty[acc], acc_phase ^ 1);
+                if (p.trace) p.trace[8 * u + 4] = global_ns();
                 tc_fence_after();
                 const uint32_t d_tmem = tmem_base + acc * kBN;
+                long long wait_cyc = 0;
                 for (int kb = 0; kb < kbs; ++kb) {
-                    mbar_wait(&full[stage], phase);
+                    if (p.trace) {
+                        const long long c0 = clock64();
+                        mbar_wait(&full[stage], phase);
+                        const long long c1 = clock64();
+                        if (kb == 0)
+                            p.trace[8 * u + 5] = global_ns();
+                        else
+                            wait_cyc += c1 - c0;
+                    } else {
+                        mbar_wait(&full[stage], phase);
+                    }
                     tc_fence_after();
                     const uint32_t a_base = smem_u32(sA + stage * kPA);
                     const uint32_t b_base = smem_u32(sB + stage * kPB);
@@ -363,7 +375,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(128 + 32 * kEpiWarps
                     }
                 }
                 umma_commit_pair(&tfull[acc], 0x3);
-                if (p.trace) p.trace[4 * u + 1] = global_ns();
+                if (p.trace) {
+                    p.trace[8 * u + 1] = global_ns();
+                    p.trace[8 * u + 6] = wait_cyc;
+                }
                 acc ^= 1;
                 if (acc == 0) acc_phase ^= 1;
             }
@@ -490,8 +505,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(128 + 32 * kEpiWarps
                 if (p.trace && rank == 0) {
                     unsigned smid;
                     asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
-                    p.trace[4 * u + 2] = global_ns();
-                    p.trace[4 * u + 3] = smid;
+                    p.trace[8 * u + 2] = global_ns();
+                    p.trace[8 * u + 3] = smid;
                 }
                 if (un.type == kUnitGrad) {
                     atomicAdd(p.counters + p.gm_base + un.c * p.mb_max + un.m_blk, 1u);

@@ -83,7 +83,8 @@ struct BwdParams {
                              // bit2: evict_last on G stores, bit3: evict_first on H loads (dW)
     int64_t nc_max, ldg, d, lddh, lddw, v_offset, ignore_index;
     unsigned* counters;      // [0] scheduler, 4 per chunk, then mb_max per chunk
-    unsigned long long* trace;  // dev only: [units][4] = MMA start, MMA end, epilogue end, smid
+    unsigned long long* trace;  // dev only: [units][8] = MMA start, MMA end, epilogue end, smid,
+                                //   accumulator free, first stage ready, stage-wait cycles
     const int64_t* targets;
     const float* lse;
     const float* gamma;

@@ -14,33 +14,30 @@ mb, vt, vm, dt = rc // 256, bc // 256, bc // 256, d // 256
 ng, nh, nw = mb * vt, mb * dt, vm * dt
 per = ng + nh + nw
 units = NR * NB * per
-tr = torch.zeros(units * 4, dtype=torch.int64, device="cuda")
+tr = torch.zeros(units * 8, dtype=torch.int64, device="cuda")
 h.set_option("trace_ptr", tr.data_ptr())
 dh = torch.empty(n, d, device="cuda")
 for _ in range(2):
+    tr.zero_()
     fce.fused_backward_recompute(H, W, Y, out.stats, "mean", 1.0, handle=h, dhidden=dh)
 torch.cuda.synchronize()
-t = tr.view(units, 4).cpu().numpy().astype(np.int64)
+t = tr.view(units, 8).cpu().numpy().astype(np.int64)
 h.set_option("trace_ptr", 0)
-l = np.arange(units) % per
+ok = (t[:, 0] > 0) & (t[:, 1] > 0) & (t[:, 2] > 0)
+t = t[ok]
+l = (np.arange(units)[ok]) % per
 typ = np.where(l < ng, 0, np.where(l < ng + nh, 1, 2))
-t0 = t[:, 0].min()
-dur_mma = (t[:, 1] - t[:, 0]) / 1e3
-dur_all = (t[:, 2] - t[:, 0]) / 1e3
 kb = np.where(typ == 0, d // 64, np.where(typ == 1, bc // 64, rc // 64))
+clk = 1.4e3  # cycles per us (approx)
 for k, name in enumerate(["grad", "dH", "dW"]):
     s = typ == k
-    print(f"{name}: units {s.sum()}  mma-issue span mean {dur_mma[s].mean():.1f} us  start->epi-end mean {dur_all[s].mean():.1f} us  "
-          f"ideal {kb[s].mean()*512/1.5e3:.1f} us  kblocks {kb[s].mean():.0f}")
-total = (t[:, 2].max() - t0) / 1e6
-print(f"backward span {total:.2f} ms")
-# per-SM busy fraction: sum of MMA spans / total
-sm = t[:, 3]
-busy = np.bincount(sm.astype(int), weights=(t[:, 1] - t[:, 0]).astype(float)) / 1e6
-busy = busy[busy > 0]
-print(f"pairs {len(busy)}  MMA-issue busy per pair: mean {busy.mean():.2f} ms, min {busy.min():.2f}, max {busy.max():.2f}")
-# gaps: for each SM, time between consecutive units' MMA start
-order = np.lexsort((t[:, 0], sm))
-ts, sms = t[order, 0], sm[order]
-gaps = np.diff(ts)[np.diff(sms) == 0] / 1e3
-print(f"start-to-start per pair: mean {gaps.mean():.1f} us median {np.median(gaps):.1f}")
+    span = (t[s, 1] - t[s, 0]) / 1e3
+    acc_wait = (t[s, 4] - t[s, 0]) / 1e3
+    first = (t[s, 5] - t[s, 4]) / 1e3
+    steady = t[s, 6] / clk
+    epi = (t[s, 2] - t[s, 1]) / 1e3
+    print(f"{name:4s}: n={s.sum():6d} span {span.mean():6.1f} us = acc-free wait {acc_wait.mean():5.1f} + first-stage {first.mean():5.1f} "
+          f"+ rest {span.mean()-acc_wait.mean()-first.mean():6.1f} (of which stage waits ~{steady.mean():5.1f});"
+          f" ideal {kb[s].mean()*512/clk:5.1f}; issue-end->epi-end {epi.mean():5.1f}")
+t0 = t[:, 0].min()
+print(f"backward span {(t[:, 2].max() - t0) / 1e6:.2f} ms")
