@@ -339,7 +339,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(128 + 32 * kEpiWarps
                 const int b_mn = un.type == kUnitGrad ? 0 : 1;
                 const uint32_t idesc = make_idesc_bf16(kPM, kBN, a_mn, b_mn);
                 const int kbs = unit_kblocks(p, un);
-                if (p.trace) p.trace[8 * u + 0] = global_ns();
+                long long cyc0 = 0;
+                if (p.trace) {
+                    p.trace[8 * u + 0] = global_ns();
+                    cyc0 = clock64();
+                }
                 mbar_wait(&tempty[acc], acc_phase ^ 1);
                 if (p.trace) p.trace[8 * u + 4] = global_ns();
                 tc_fence_after();
@@ -378,6 +382,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(128 + 32 * kEpiWarps
                 if (p.trace) {
                     p.trace[8 * u + 1] = global_ns();
                     p.trace[8 * u + 6] = wait_cyc;
+                    p.trace[8 * u + 7] = clock64() - cyc0;
                 }
                 acc ^= 1;
                 if (acc == 0) acc_phase ^= 1;

@@ -28,7 +28,9 @@ t = t[ok]
 l = (np.arange(units)[ok]) % per
 typ = np.where(l < ng, 0, np.where(l < ng + nh, 1, 2))
 kb = np.where(typ == 0, d // 64, np.where(typ == 1, bc // 64, rc // 64))
-clk = 1.4e3  # cycles per us (approx)
+span_ns = (t[:, 1] - t[:, 0]).astype(float)
+clk = float(np.median(t[:, 7] / np.maximum(span_ns, 1))) * 1e3  # SM cycles per us, measured
+print(f"measured SM clock during the backward: {clk:.0f} MHz")
 for k, name in enumerate(["grad", "dH", "dW"]):
     s = typ == k
     span = (t[s, 1] - t[s, 0]) / 1e3
