@@ -633,7 +633,7 @@ fce_status fce_backward(fce_handle h, const fce_problem* p, fce_stats stats, int
     int64_t band = h->band_cols;
     if (!band) {
         // ~32 MB of G per chunk so it stays L2 resident between producer and consumers
-        band = h->bwd_persistent ? 2048
+        band = h->bwd_persistent ? 3072
                                  : std::max<int64_t>(kBN, ((int64_t(16) << 20) / row_chunk) / kBN * kBN);
     }
     band = std::min(band, round_up(p->v, kBN));

@@ -453,10 +453,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(128 + 32 * kEpiWarps
                                 packed[j >> 1] = pack_bf16(g0, g1);
                             }
                             __nv_bfloat16* dst = grow_ptr + col0;
-#pragma unroll
-                            for (int j = 0; j < 4; ++j)
-                                st_v4_b32_hint(dst + 8 * j, packed[4 * j], packed[4 * j + 1],
-                                               packed[4 * j + 2], packed[4 * j + 3], pol_gst);
+                            st_v8_b32_hint(dst, packed, pol_gst);
+                            st_v8_b32_hint(dst + 16, packed + 8, pol_gst);
                         }
                     }
                 } else {
@@ -480,6 +478,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(128 + 32 * kEpiWarps
 #pragma unroll
                                     for (int j = 0; j < 32; j += 4)
                                         red_add_v4_hint(dst + j, v[j], v[j + 1], v[j + 2], v[j + 3], pol_out);
+                                } else if ((reinterpret_cast<uintptr_t>(dst) & 31) == 0) {
+#pragma unroll
+                                    for (int j = 0; j < 32; j += 8) st_v8_f32_hint(dst + j, v + j, pol_out);
                                 } else {
 #pragma unroll
                                     for (int j = 0; j < 32; j += 4)

@@ -194,6 +194,21 @@ __device__ __forceinline__ void st_v4_b32_hint(void* addr, uint32_t a, uint32_t 
                  : "memory");
 }
 
+// 256-bit stores (sm_100): one full 32-byte sector per thread per instruction
+__device__ __forceinline__ void st_v8_b32_hint(void* addr, const uint32_t* v, uint64_t pol) {
+    asm volatile("st.global.L2::cache_hint.v8.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8}, %9;" ::"l"(addr),
+                 "r"(v[0]), "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7]),
+                 "l"(pol)
+                 : "memory");
+}
+
+__device__ __forceinline__ void st_v8_f32_hint(float* addr, const float* v, uint64_t pol) {
+    asm volatile("st.global.L2::cache_hint.v8.f32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8}, %9;" ::"l"(addr),
+                 "f"(v[0]), "f"(v[1]), "f"(v[2]), "f"(v[3]), "f"(v[4]), "f"(v[5]), "f"(v[6]), "f"(v[7]),
+                 "l"(pol)
+                 : "memory");
+}
+
 __device__ __forceinline__ uint64_t policy_evict_first() {
     uint64_t q;
     asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(q));
