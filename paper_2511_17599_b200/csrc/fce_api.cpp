@@ -57,7 +57,8 @@ struct fce_handle_s {
     int64_t gemm_pair = 1;
     int64_t bwd_unit_mask = 7;
     int64_t trace_ptr = 0;
-    int64_t bwd_epi_warps = 8;  // dev only: device buffer for per-unit timestamps
+    int64_t bwd_epi_warps = 8;
+    int64_t bwd_tma_epi = 1;  // dev only: device buffer for per-unit timestamps
     int64_t launches = 0;
     size_t bwd_scratch[4] = {0, 0, 0, 0};  // offsets of the persistent-backward scratch
     // optional per-kernel CUDA-event timing of the tile kernels (bench roofline)
@@ -339,6 +340,15 @@ fce_status run_backward_persistent(fce_handle h, const fce_problem* p, const flo
         !encode_map_2d(&maps.h_mn, p->hidden, p->d, p->n, p->ldh * 2, 64, 64))
         return fail(FCE_CUDA_ERROR, "cuTensorMapEncodeTiled failed (persistent backward)");
 
+    // epilogue through SMEM + TMA store / reduce-add when the outputs allow
+    // TMA (16-byte aligned rows); otherwise per-thread vector stores
+    bp.tma_epi = 0;
+    if (h->bwd_tma_epi) {
+        bool ok = encode_map_2d(&maps.g_st, g_ring, band, ring_rows, band * 2, 64, 128);
+        if (ok && dhidden) ok = encode_map_2d(&maps.dh_st, dhidden, p->d, p->n, lddh * 4, 32, 128, true);
+        if (ok && dweight) ok = encode_map_2d(&maps.dw_st, dweight, p->d, p->v, lddw * 4, 32, 128, true);
+        bp.tma_epi = ok ? 1 : 0;
+    }
     cudaEvent_t e0 = nullptr, e1 = nullptr;
     if (h->timing) {
         e0 = pool_event(h);
@@ -450,6 +460,8 @@ fce_status fce_set_option(fce_handle h, const char* key, int64_t value) {
         h->row_chunk = value;
     } else if (!std::strcmp(key, "validate")) {
         h->validate = value ? 1 : 0;
+    } else if (!std::strcmp(key, "bwd_tma_epi")) {
+        h->bwd_tma_epi = value ? 1 : 0;
     } else if (!std::strcmp(key, "bwd_epi_warps")) {
         if (value != 4 && value != 8) return fail(FCE_INVALID_ARGUMENT, "bwd_epi_warps must be 4 or 8");
         h->bwd_epi_warps = value;

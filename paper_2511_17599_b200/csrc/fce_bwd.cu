@@ -46,6 +46,7 @@ constexpr int kPS = 6;                     // pipeline stages
 constexpr int kPA = 128 * kBK * 2;         // this CTA's A rows per stage
 constexpr int kPB = 128 * kBK * 2;         // this CTA's B columns per stage
 constexpr int kPM = 256;                   // unit rows (pair)
+constexpr int kEpiStage = 2 * 16384;       // epilogue staging: one 128-row x 128-byte slice per column group
 // epilogue warps: 4 (one per TMEM lane quarter, 256 columns each) or 8 (two per
 // quarter, 128 columns each); selected at launch (option "bwd_epi_warps")
 
@@ -147,7 +148,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(128 + 32 * kEpiWarps
     uint8_t* smem = smem_raw + (((raw_addr + 1023u) & ~1023u) - raw_addr);
     uint8_t* sA = smem;
     uint8_t* sB = smem + kPS * kPA;
-    uint64_t* bars = reinterpret_cast<uint64_t*>(sB + kPS * kPB);
+    uint8_t* sEpi = sB + kPS * kPB;  // 2 x 16 KB epilogue staging (TMA store / reduce-add)
+    uint64_t* bars = reinterpret_cast<uint64_t*>(sEpi + kEpiStage);
     uint64_t* full = bars;
     uint64_t* empty = bars + kPS;
     uint64_t* tfull = bars + 2 * kPS;
@@ -421,7 +423,96 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(128 + 32 * kEpiWarps
                 const uint32_t taddr = tmem_base + (static_cast<uint32_t>(q * 32) << 16) +
                                        static_cast<uint32_t>(acc * kBN);
                 const int lrow = un.m_blk * kPM + static_cast<int>(rank) * 128 + r;
-                if (un.type == kUnitGrad) {
+                if (p.tma_epi) {
+                    // Each column group (4 warps, one TMEM lane quarter each) stages a
+                    // 128-row x 128-byte slice in swizzled SMEM and one thread hands it
+                    // to the TMA engine: full-line stores / reduce-adds instead of 32
+                    // scattered 16-byte requests per warp instruction.
+                    const int grp = warp >> 2;
+                    const bool gl = (threadIdx.x & 127) == 0;  // group leader
+                    const uint32_t sbuf = smem_u32(sEpi + grp * 16384);
+                    const int ncols = kBN / (kEpiWarps / 4);
+                    const int gcol0 = grp * ncols;
+                    const uint32_t my_row = sbuf + static_cast<uint32_t>(r) * 128u;
+                    const uint32_t sw = static_cast<uint32_t>(r & 7);
+                    if (un.type == kUnitGrad) {
+                        const bool row_ok = lrow < un.nc;
+                        const int64_t grow = static_cast<int64_t>(un.r0) + lrow;
+                        float gam = 0.f, l2lse = 0.f;
+                        int64_t tcol = -1;
+                        if (row_ok) {
+                            const int64_t y = p.targets[grow];
+                            const bool skip = p.has_ignore && y == p.ignore_index;
+                            gam = skip ? 0.f : p.gamma[grow];
+                            l2lse = skip ? 0.f : p.lse[grow] * kL2e;
+                            tcol = y - (p.v_offset + un.vb);
+                        }
+#pragma unroll 1
+                        for (int sl = 0; sl < ncols / 64; ++sl) {
+                            const int c64 = gcol0 + sl * 64;
+                            if (gl) bulk_wait_read0();
+                            named_bar_sync(2 + grp, 128);
+                            uint32_t packed[32];
+#pragma unroll
+                            for (int h2 = 0; h2 < 2; ++h2) {
+                                float v[32];
+                                tmem_ld32(taddr + c64 + h2 * 32, v);
+                                const int col0 = un.n_tile * kBN + c64 + h2 * 32;
+                                const int64_t tc = tcol - col0;
+#pragma unroll
+                                for (int j = 0; j < 32; j += 2) {
+                                    float g0 = gam * (ex2(fmaf(v[j], kL2e, -l2lse)) - (tc == j ? 1.f : 0.f));
+                                    float g1 = gam * (ex2(fmaf(v[j + 1], kL2e, -l2lse)) - (tc == j + 1 ? 1.f : 0.f));
+                                    if (gam == 0.f || col0 + j >= un.vc) g0 = 0.f;
+                                    if (gam == 0.f || col0 + j + 1 >= un.vc) g1 = 0.f;
+                                    packed[h2 * 16 + (j >> 1)] = pack_bf16(g0, g1);
+                                }
+                            }
+#pragma unroll
+                            for (int ch = 0; ch < 8; ++ch)
+                                st_shared_v4(my_row + ((static_cast<uint32_t>(ch) ^ sw) << 4), packed[4 * ch],
+                                             packed[4 * ch + 1], packed[4 * ch + 2], packed[4 * ch + 3]);
+                            fence_proxy_async_shared();
+                            named_bar_sync(2 + grp, 128);
+                            if (gl) {
+                                tma_store_2d(&maps.g_st, sbuf, un.n_tile * kBN + c64,
+                                             un.slot * static_cast<int>(p.nc_max) + un.m_blk * kPM +
+                                                 static_cast<int>(rank) * 128);
+                                bulk_commit();
+                            }
+                        }
+                    } else {
+                        const bool is_dh = un.type == kUnitDH;
+                        const bool accumulate = is_dh ? (un.band_idx > 0 || p.accumulate_dh) : (un.row_idx > 0);
+                        const CUtensorMap* om = is_dh ? &maps.dh_st : &maps.dw_st;
+                        const int orow = (is_dh ? un.r0 : un.vb) + un.m_blk * kPM + static_cast<int>(rank) * 128;
+                        const bool discard = (p.unit_mask >> 5) & 1;
+#pragma unroll 1
+                        for (int sl = 0; sl < ncols / 32; ++sl) {
+                            const int c32 = gcol0 + sl * 32;
+                            if (gl) bulk_wait_read0();
+                            named_bar_sync(2 + grp, 128);
+                            float v[32];
+                            tmem_ld32(taddr + c32, v);
+                            const uint32_t* vu = reinterpret_cast<const uint32_t*>(v);
+#pragma unroll
+                            for (int ch = 0; ch < 8; ++ch)
+                                st_shared_v4(my_row + ((static_cast<uint32_t>(ch) ^ sw) << 4), vu[4 * ch],
+                                             vu[4 * ch + 1], vu[4 * ch + 2], vu[4 * ch + 3]);
+                            fence_proxy_async_shared();
+                            named_bar_sync(2 + grp, 128);
+                            if (gl && !discard) {
+                                if (accumulate)
+                                    tma_reduce_add_2d(om, sbuf, un.n_tile * kBN + c32, orow);
+                                else
+                                    tma_store_2d(om, sbuf, un.n_tile * kBN + c32, orow);
+                                bulk_commit();
+                            }
+                        }
+                    }
+                    // the unit's writes must be complete before its completion is published
+                    if (gl) bulk_wait_all0();
+                } else if (un.type == kUnitGrad) {
                     const bool row_ok = lrow < un.nc;
                     const int64_t grow = static_cast<int64_t>(un.r0) + lrow;
                     float gam = 0.f, l2lse = 0.f;
@@ -539,7 +630,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(128 + 32 * kEpiWarps
     if (warp == kWarpAlloc) tmem_dealloc_pair<512>(tmem_base);
 }
 
-constexpr int kBwdSmem = kPS * (kPA + kPB) + 1024 + 512;
+constexpr int kBwdSmem = kPS * (kPA + kPB) + kEpiStage + 1024 + 512;
 
 cudaError_t launch_bwd_persistent(const BwdParams& p, const BwdMaps& maps, int grid,
                                   cudaStream_t stream) {

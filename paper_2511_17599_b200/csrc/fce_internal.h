@@ -79,6 +79,7 @@ struct BwdParams {
     int has_ignore, accumulate_dh;
     int unit_mask;           // debug / profiling: bit0 grad, bit1 dH, bit2 dW units do work
     int epi_warps;           // 4 or 8 epilogue warps per CTA
+    int tma_epi;             // 1: epilogue writes G / dH / dW through SMEM + TMA store / reduce-add
     int l2_hints;            // bit0: evict_first on dH/dW writes, bit1: evict_last on G loads,
                              // bit2: evict_last on G stores, bit3: evict_first on H loads (dW)
     int64_t nc_max, ldg, d, lddh, lddw, v_offset, ignore_index;
@@ -95,6 +96,7 @@ struct BwdParams {
 
 struct BwdMaps {
     CUtensorMap h_k, w_k, g_k, w_mn, g_mn, h_mn;
+    CUtensorMap g_st, dh_st, dw_st;  // epilogue TMA stores / reduce-adds (tma_epi)
 };
 
 cudaError_t launch_pair_gemm(const GemmProblem& q, const TensorMaps& maps, int sms,
@@ -110,7 +112,8 @@ void set_last_error(const char* msg);
 
 // Host helpers (fce_kernels.cu)
 bool encode_map_2d(CUtensorMap* map, const void* base, uint64_t inner, uint64_t outer,
-                   uint64_t row_stride_bytes, uint32_t box_inner, uint32_t box_outer);
+                   uint64_t row_stride_bytes, uint32_t box_inner, uint32_t box_outer,
+                   bool fp32 = false);
 cudaError_t launch_tile_kernel(const TileParams& p, const TensorMaps& maps, int grid,
                                cudaStream_t stream);
 int device_sm_count(int device);
