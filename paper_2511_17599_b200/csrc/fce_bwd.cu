@@ -246,17 +246,21 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(128 + 32 * kEpiWarps
         }
     } else if (warp == kWarpTma) {
         // ------------------------------------------------ TMA producer (both CTAs)
-        if (lane == 0) {
+        // Whole warp, converged; one elected lane issues each TMA.
+        {
             int stage = 0, us = 0;
             uint32_t phase = 0, uphase = 0;
             const uint64_t pol_norm = policy_evict_normal();
             const uint64_t pol_g = (p.l2_hints & 2) ? policy_evict_last() : pol_norm;
             const uint64_t pol_h = (p.l2_hints & 8) ? policy_evict_first() : pol_norm;
             const uint32_t leader_full0 = mapa_shared(&full[0], 0);
+            const uint32_t sa0 = smem_u32(sA), sb0 = smem_u32(sB);
             for (;;) {
                 mbar_wait_cluster(&ufull[us], uphase);
                 const int u = unit_ring[us];
-                mbar_arrive_cluster(leader_uempty0 + 8 * us);
+                __syncwarp();
+                if (lane == 0) mbar_arrive_cluster(leader_uempty0 + 8 * us);
+                __syncwarp();
                 if (++us == kUnitRing) {
                     us = 0;
                     uphase ^= 1;
@@ -301,23 +305,21 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(128 + 32 * kEpiWarps
                 const int kbs = unit_kblocks(p, un);
                 for (int kb = 0; kb < kbs; ++kb) {
                     mbar_wait(&empty[stage], phase ^ 1);
-                    if (rank == 0) mbar_arrive_expect_tx(&full[stage], 2 * (kPA + kPB));
+                    if (rank == 0) mbar_arrive_expect_tx_w(&full[stage], 2 * (kPA + kPB));
                     const uint32_t fb = leader_full0 + stage * 8;
-                    uint8_t* a_dst = sA + stage * kPA;
-                    uint8_t* b_dst = sB + stage * kPB;
+                    const uint32_t a_dst = sa0 + stage * kPA;
+                    const uint32_t b_dst = sb0 + stage * kPB;
                     if (!a_mn) {
-                        tma_load_2d_pair(a_dst, ma, fb, a_k0 + kb * kBK, a_row, pa);
+                        tma_load_2d_pair_w(a_dst, ma, fb, a_k0 + kb * kBK, a_row, pa);
                     } else {
-#pragma unroll
-                        for (int j = 0; j < 2; ++j)
-                            tma_load_2d_pair(a_dst + j * 8192, ma, fb, a_row + 64 * j, a_k0 + kb * kBK, pa);
+                        tma_load_2d_pair_w(a_dst, ma, fb, a_row, a_k0 + kb * kBK, pa);
+                        tma_load_2d_pair_w(a_dst + 8192, ma, fb, a_row + 64, a_k0 + kb * kBK, pa);
                     }
                     if (!b_mn) {
-                        tma_load_2d_pair(b_dst, mb, fb, b_k0 + kb * kBK, b_row, pb);
+                        tma_load_2d_pair_w(b_dst, mb, fb, b_k0 + kb * kBK, b_row, pb);
                     } else {
-#pragma unroll
-                        for (int j = 0; j < 2; ++j)
-                            tma_load_2d_pair(b_dst + j * 8192, mb, fb, b_row + 64 * j, b_k0 + kb * kBK, pb);
+                        tma_load_2d_pair_w(b_dst, mb, fb, b_row, b_k0 + kb * kBK, pb);
+                        tma_load_2d_pair_w(b_dst + 8192, mb, fb, b_row + 64, b_k0 + kb * kBK, pb);
                     }
                     if (++stage == kPS) {
                         stage = 0;
@@ -328,13 +330,19 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(128 + 32 * kEpiWarps
         }
     } else if (warp == kWarpMma) {
         // ------------------------------------------------ MMA issuer (even CTA)
-        if (lane == 0 && rank == 0) {
+        // The whole warp runs the loop (converged, warp-uniform operands) and
+        // one elected lane issues, so each MMA is a single UTCHMMA.2CTA; the
+        // descriptors of every (stage, k) are a fixed offset from the unit's base.
+        if (rank == 0) {
             int stage = 0, us = 0, acc = 0;
             uint32_t phase = 0, uphase = 0, acc_phase = 0;
+            const uint32_t sa0 = smem_u32(sA), sb0 = smem_u32(sB);
             for (;;) {
                 mbar_wait(&ufull[us], uphase);
                 const int u = unit_ring[us];
-                mbar_arrive(&uempty[us]);
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&uempty[us]);
+                __syncwarp();
                 if (++us == kUnitRing) {
                     us = 0;
                     uphase ^= 1;
@@ -342,17 +350,22 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(128 + 32 * kEpiWarps
                 const BUnit un = decode_unit(p, u);
                 if (un.type == kUnitStop) break;
                 if (un.empty) continue;
-                const int a_mn = un.type == kUnitDW ? 1 : 0;
-                const int b_mn = un.type == kUnitGrad ? 0 : 1;
+                const uint32_t a_mn = un.type == kUnitDW ? 1u : 0u;
+                const uint32_t b_mn = un.type == kUnitGrad ? 0u : 1u;
                 const uint32_t idesc = make_idesc_bf16(kPM, kBN, a_mn, b_mn);
+                // descriptor of stage 0, k 0 and the per-k step (in 16-byte units)
+                const uint64_t ad0 = a_mn ? make_sdesc_sw128(sa0, 8192, 1024) : make_sdesc_sw128(sa0, 16, 1024);
+                const uint64_t bd0 = b_mn ? make_sdesc_sw128(sb0, 8192, 1024) : make_sdesc_sw128(sb0, 16, 1024);
+                const uint32_t astep = a_mn ? (2048u >> 4) : (32u >> 4);
+                const uint32_t bstep = b_mn ? (2048u >> 4) : (32u >> 4);
                 const int kbs = unit_kblocks(p, un);
                 long long cyc0 = 0;
-                if (p.trace) {
+                if (p.trace && lane == 0) {
                     p.trace[8 * u + 0] = global_ns();
                     cyc0 = clock64();
                 }
                 mbar_wait(&tempty[acc], acc_phase ^ 1);
-                if (p.trace) p.trace[8 * u + 4] = global_ns();
+                if (p.trace && lane == 0) p.trace[8 * u + 4] = global_ns();
                 tc_fence_after();
                 const uint32_t d_tmem = tmem_base + acc * kBN;
                 long long wait_cyc = 0;
@@ -361,32 +374,28 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(128 + 32 * kEpiWarps
                         const long long c0 = clock64();
                         mbar_wait(&full[stage], phase);
                         const long long c1 = clock64();
-                        if (kb == 0)
-                            p.trace[8 * u + 5] = global_ns();
-                        else
+                        if (kb == 0) {
+                            if (lane == 0) p.trace[8 * u + 5] = global_ns();
+                        } else {
                             wait_cyc += c1 - c0;
+                        }
                     } else {
                         mbar_wait(&full[stage], phase);
                     }
                     tc_fence_after();
-                    const uint32_t a_base = smem_u32(sA + stage * kPA);
-                    const uint32_t b_base = smem_u32(sB + stage * kPB);
+                    const uint64_t ads = ad0 + static_cast<uint64_t>((stage * kPA) >> 4);
+                    const uint64_t bds = bd0 + static_cast<uint64_t>((stage * kPB) >> 4);
 #pragma unroll
-                    for (int k = 0; k < kBK / 16; ++k) {
-                        const uint64_t ad = a_mn ? make_sdesc_sw128(a_base + k * 2048, 8192, 1024)
-                                                 : make_sdesc_sw128(a_base + k * 32, 16, 1024);
-                        const uint64_t bd = b_mn ? make_sdesc_sw128(b_base + k * 2048, 8192, 1024)
-                                                 : make_sdesc_sw128(b_base + k * 32, 16, 1024);
-                        umma_bf16_pair(d_tmem, ad, bd, idesc, (kb | k) != 0 ? 1u : 0u);
-                    }
-                    umma_commit_pair(&empty[stage], 0x3);
+                    for (int k = 0; k < kBK / 16; ++k)
+                        umma_bf16_pair_w(d_tmem, ads + k * astep, bds + k * bstep, idesc, (kb | k) != 0 ? 1u : 0u);
+                    umma_commit_pair_w(&empty[stage], 0x3);
                     if (++stage == kPS) {
                         stage = 0;
                         phase ^= 1;
                     }
                 }
-                umma_commit_pair(&tfull[acc], 0x3);
-                if (p.trace) {
+                umma_commit_pair_w(&tfull[acc], 0x3);
+                if (p.trace && lane == 0) {
                     p.trace[8 * u + 1] = global_ns();
                     p.trace[8 * u + 6] = wait_cyc;
                     p.trace[8 * u + 7] = clock64() - cyc0;
