@@ -124,9 +124,12 @@ __global__ void __launch_bounds__(kThreads, 1)
 
     if (warp == 0) {
         // ------------------------------------------------------------ TMA producer
-        if (lane == 0) {
+        // Whole warp, converged, warp-uniform operands; one elected lane issues
+        // (a single UTMALDG per load instead of an ELECT / BRA.U.ANY loop).
+        {
             int stage = 0;
             uint32_t phase = 0;
+            const uint32_t sa0 = smem_u32(sA), sb0 = smem_u32(sB);
             for (int u = blockIdx.x; u < p.units; u += gridDim.x) {
                 const Unit un = get_unit(p, u);
                 const CUtensorMap* ma = un.prob ? &maps.a1 : &maps.a0;
@@ -141,26 +144,24 @@ __global__ void __launch_bounds__(kThreads, 1)
                     const int n_tile = un.n_tile0 + t;
                     for (int kb = 0; kb < kbs; ++kb) {
                         mbar_wait(&empty[stage], phase ^ 1);
-                        mbar_arrive_expect_tx(&full[stage], kStageBytesA + kStageBytesB);
-                        uint8_t* a_dst = sA + stage * kStageBytesA;
-                        uint8_t* b_dst = sB + stage * kStageBytesB;
+                        mbar_arrive_expect_tx_w(&full[stage], kStageBytesA + kStageBytesB);
+                        const uint32_t a_dst = sa0 + stage * kStageBytesA;
+                        const uint32_t b_dst = sb0 + stage * kStageBytesB;
                         if (!a_mn) {
-                            tma_load_2d(a_dst, ma, &full[stage], kb * kBK, un.m_blk * kBM,
-                                        kEvictNormal);
+                            tma_load_2d_w(a_dst, ma, &full[stage], kb * kBK, un.m_blk * kBM, kEvictNormal);
                         } else {
 #pragma unroll
                             for (int j = 0; j < kBM / 64; ++j)
-                                tma_load_2d(a_dst + j * 8192, ma, &full[stage],
-                                            un.m_blk * kBM + 64 * j, kb * kBK, kEvictNormal);
+                                tma_load_2d_w(a_dst + j * 8192, ma, &full[stage], un.m_blk * kBM + 64 * j, kb * kBK,
+                                              kEvictNormal);
                         }
                         if (!b_mn) {
-                            tma_load_2d(b_dst, mb, &full[stage], kb * kBK, n_tile * kBN,
-                                        kEvictNormal);
+                            tma_load_2d_w(b_dst, mb, &full[stage], kb * kBK, n_tile * kBN, kEvictNormal);
                         } else {
 #pragma unroll
                             for (int j = 0; j < kBN / 64; ++j)
-                                tma_load_2d(b_dst + j * 8192, mb, &full[stage],
-                                            n_tile * kBN + 64 * j, kb * kBK, kEvictNormal);
+                                tma_load_2d_w(b_dst + j * 8192, mb, &full[stage], n_tile * kBN + 64 * j, kb * kBK,
+                                              kEvictNormal);
                         }
                         if (++stage == kStages) {
                             stage = 0;
@@ -172,20 +173,29 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
     } else if (warp == 1) {
         // ------------------------------------------------------------ MMA issuer
-        if (lane == 0) {
+        {
             int stage = 0;
             uint32_t phase = 0;
             int acc = 0;
             uint32_t acc_phase = 0;
+            const uint32_t sa0 = smem_u32(sA), sb0 = smem_u32(sB);
             for (int u = blockIdx.x; u < p.units; u += gridDim.x) {
                 const Unit un = get_unit(p, u);
-                int kbs = p.k_blocks, a_mn = 0, b_mn = 0;
+                int kbs = p.k_blocks;
+                uint32_t a_mn = 0, b_mn = 0;
                 if (EPI == kEpiGemm) {
                     kbs = p.prob[un.prob].k_blocks;
                     a_mn = p.prob[un.prob].a_mn;
                     b_mn = p.prob[un.prob].b_mn;
                 }
                 const uint32_t idesc = make_idesc_bf16(kBM, kBN, a_mn, b_mn);
+                // K-major SW128: +32 B per K=16 step inside the 128-B atom.
+                // MN-major SW128: +16 rows * 128 B = 2 KB per K=16 step; LBO = 8 KB
+                // between 64-wide M/N column blocks.
+                const uint64_t ad0 = a_mn ? make_sdesc_sw128(sa0, 8192, 1024) : make_sdesc_sw128(sa0, 16, 1024);
+                const uint64_t bd0 = b_mn ? make_sdesc_sw128(sb0, 8192, 1024) : make_sdesc_sw128(sb0, 16, 1024);
+                const uint32_t astep = a_mn ? (2048u >> 4) : (32u >> 4);
+                const uint32_t bstep = b_mn ? (2048u >> 4) : (32u >> 4);
                 for (int t = 0; t < un.n_tiles; ++t) {
                     mbar_wait(&tempty[acc], acc_phase ^ 1);
                     tc_fence_after();
@@ -193,26 +203,18 @@ __global__ void __launch_bounds__(kThreads, 1)
                     for (int kb = 0; kb < kbs; ++kb) {
                         mbar_wait(&full[stage], phase);
                         tc_fence_after();
-                        const uint32_t a_base = smem_u32(sA + stage * kStageBytesA);
-                        const uint32_t b_base = smem_u32(sB + stage * kStageBytesB);
+                        const uint64_t ads = ad0 + static_cast<uint64_t>((stage * kStageBytesA) >> 4);
+                        const uint64_t bds = bd0 + static_cast<uint64_t>((stage * kStageBytesB) >> 4);
 #pragma unroll
-                        for (int k = 0; k < kBK / 16; ++k) {
-                            // K-major SW128: +32 B per K=16 step inside the 128-B atom.
-                            // MN-major SW128: +16 rows * 128 B = 2 KB per K=16 step;
-                            //   LBO = 8 KB between 64-wide M/N column blocks.
-                            const uint64_t ad = a_mn ? make_sdesc_sw128(a_base + k * 2048, 8192, 1024)
-                                                     : make_sdesc_sw128(a_base + k * 32, 16, 1024);
-                            const uint64_t bd = b_mn ? make_sdesc_sw128(b_base + k * 2048, 8192, 1024)
-                                                     : make_sdesc_sw128(b_base + k * 32, 16, 1024);
-                            umma_bf16(d_tmem, ad, bd, idesc, (kb | k) != 0 ? 1u : 0u);
-                        }
-                        umma_commit(&empty[stage]);
+                        for (int k = 0; k < kBK / 16; ++k)
+                            umma_bf16_w(d_tmem, ads + k * astep, bds + k * bstep, idesc, (kb | k) != 0 ? 1u : 0u);
+                        umma_commit_w(&empty[stage]);
                         if (++stage == kStages) {
                             stage = 0;
                             phase ^= 1;
                         }
                     }
-                    umma_commit(&tfull[acc]);
+                    umma_commit_w(&tfull[acc]);
                     acc ^= 1;
                     if (acc == 0) acc_phase ^= 1;
                 }
