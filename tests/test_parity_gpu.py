@@ -418,33 +418,47 @@ def test_native_vocab_parallel_single_rank(cuda):
 
 # ------------------------------------------------------------------ full size
 
+FULL_CONFIGS = [
+    # BASELINE.json configs[1:] at full size
+    ("llama3-8b", 16384, 4096, 128256, 0.0),
+    ("qwen2.5-7b", 32768, 3584, 152064, 0.25),
+    ("gemma2-2b", 65536, 2304, 256000, 0.0),
+    ("llama3-70b", 131072, 8192, 128256, 0.0),
+]
+
+
 @pytest.mark.slow
-def test_llama3_8b_shape_properties(cuda):
-    """BASELINE configs[1] at full size (N=16384, D=4096, V=128256): a row slice
-    against the oracle, plus size-independent properties of the whole result."""
-    n, d, v = 16384, 4096, 128256
-    Hd, Wd, Yd = fce.generate_instance(n, d, v, 42)
-    out = fce.fused_forward(Hd, Wd, Yd, "sum")
-    assert torch.all(out.stats.found == 1)
-    lse = out.lse
-    assert torch.isfinite(lse).all()
-    assert abs(out.loss.item() / n - math.log(v)) < 0.05  # ~uniform logits
-    # row slice vs oracle at full D, V (rows are independent)
-    rows_idx = [0, 1, 4097, 16383]
+@pytest.mark.parametrize("name,n,d,v,frac", FULL_CONFIGS, ids=[c[0] for c in FULL_CONFIGS])
+def test_full_size_configs(cuda, name, n, d, v, frac):
+    """Every BASELINE.json config at full size: a row slice against the oracle,
+    plus size-independent properties of the whole result."""
+    ign = -100 if frac > 0 else None
+    Hd, Wd, Yd = fce.generate_instance(n, d, v, 42, -100, frac)
+    out = fce.fused_forward(Hd, Wd, Yd, "sum", ign)
+    valid = (Yd != -100) if ign is not None else torch.ones_like(Yd, dtype=torch.bool)
+    assert torch.equal(out.stats.found.bool(), valid)  # exactly the non-ignored rows
+    assert torch.isfinite(out.lse[valid]).all()
+    n_valid = int(valid.sum())
+    assert abs(out.loss.item() / n_valid - math.log(v)) < 0.05  # ~uniform logits
+    # row slice vs the oracle at full D, V (rows are independent)
+    rows_idx = [0, 1, n // 2 + 1, n - 1]
     Hs = Hd[rows_idx].float().cpu().numpy()
     Ys = Yd[rows_idx].cpu().numpy()
     Wn = Wd.float().cpu().numpy()
-    st, rows, _ = ob.forward(Hs, Wn, Ys, "none")
+    st, rows, _ = ob.forward(Hs, Wn, Ys, "none", ign)
     np.testing.assert_array_equal(out.stats.found[rows_idx].cpu().numpy(), st["found"])
     got = out.loss_rows[rows_idx].cpu().numpy()
-    assert np.max(np.abs(got - rows) / np.abs(rows)) < LOSS_RTOL
-    dh, dw = fce.fused_backward_recompute(Hd, Wd, Yd, out.stats, "sum", 1.0)
+    assert np.max(np.abs(got - rows) / np.maximum(1.0, np.abs(rows))) < LOSS_RTOL
+    dh, dw = fce.fused_backward_recompute(Hd, Wd, Yd, out.stats, "sum", 1.0, ign)
     # dH rows depend only on their own row: compare the slice to the oracle
-    dH_ref, _ = ob.backward(Hs, Wn, Ys, st, "sum", 1.0, want_dw=False)
+    dH_ref, _ = ob.backward(Hs, Wn, Ys, st, "sum", 1.0, ign, want_dw=False)
+    del Wn
     assert relmax(dh[rows_idx].cpu().numpy(), dH_ref) < GRAD_RTOL
+    if ign is not None:
+        assert torch.count_nonzero(dh[~valid]).item() == 0
     # sum_v G[n, v] = 0 per row => dW columns sum to ~0 (test_reference.cpp:218-233)
     col = dw.double().sum(0)
     assert col.abs().max().item() < 1e-3 * dw.abs().max().item() * math.sqrt(v)
     # linearity: upstream 2 doubles both gradients exactly
-    dh2, dw2 = fce.fused_backward_recompute(Hd, Wd, Yd, out.stats, "sum", 2.0)
+    dh2, dw2 = fce.fused_backward_recompute(Hd, Wd, Yd, out.stats, "sum", 2.0, ign)
     assert torch.equal(dh2, 2 * dh) and torch.equal(dw2, 2 * dw)
