@@ -200,6 +200,8 @@ def main():
     ap.add_argument("--ref-warmup", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=6)
+    ap.add_argument("--force-vp", action="store_true",
+                    help="use the native vocab-parallel (NCCL) path even on one rank (testing)")
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference_arm(args)
@@ -217,7 +219,7 @@ def main():
         raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}")
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
-    if world > 1:
+    if world > 1 or args.force_vp:
         dist.init_process_group("nccl", device_id=dev)
     n, d, v, frac = CONFIGS[args.config]
     ign = -100 if frac > 0 else None
@@ -229,7 +231,7 @@ def main():
     H, W, Y = fce.generate_instance(n, d, v, SEED, -100, frac, device=local, handle=h)
     lo, hi = fce.shard_ranges(v, world)[rank]
     Ws = W[lo:hi]
-    comm = vp.NativeComm.from_torch_distributed(local) if world > 1 else None
+    comm = vp.NativeComm.from_torch_distributed(local) if (world > 1 or args.force_vp) else None
 
     dh = torch.empty(n, d, dtype=torch.float32, device=dev)
     dw = torch.empty(hi - lo, d, dtype=torch.float32, device=dev)
@@ -255,7 +257,7 @@ def main():
 
     def barrier():
         torch.cuda.synchronize(dev)
-        if world > 1:
+        if dist.is_initialized():
             dist.barrier()
         torch.cuda.synchronize(dev)
 
@@ -357,7 +359,7 @@ def main():
     d2h = 4
 
     if rank != 0:
-        if world > 1:
+        if dist.is_initialized():
             dist.barrier()
             dist.destroy_process_group()
         return 0
@@ -403,7 +405,7 @@ def main():
         "data": "synthetic: reference splitmix64 instance (seed 42) generated on device, bf16 grid",
         "config": {"workload": CONFIG_LABEL[args.config], "N": n, "D": d, "V": v,
                    "reduction": "mean", "ignore_fraction": frac,
-                   "parallelism": f"vocab-parallel x{world}" if world > 1 else "single GPU",
+                   "parallelism": f"vocab-parallel x{world}" if comm is not None else "single GPU",
                    "l2": "inputs larger than L2 (W bf16 = %.2f GB)" % (v * d * 2 / 1e9)},
         "tflops_8ndv": flops_step / (ms_step / 1e3) / 1e12,
         "pct_peak_step": flops_step / (ms_step / 1e3) / 1e12 / peaks["bf16_tflops"],
@@ -434,7 +436,7 @@ def main():
             line["cpu_baseline"] = {"value": None, "unit": "tokens/s", "cores": os.cpu_count(),
                                     "kind": "reference", "sample": f"failed: {exc!r}"}
     print(json.dumps(line), flush=True)
-    if world > 1:
+    if dist.is_initialized():
         dist.barrier()
         dist.destroy_process_group()
     return 0
