@@ -27,6 +27,8 @@ import time
 
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
+# rank 0 must print exactly one JSON line on stdout: keep NCCL's banner off it
+os.environ.setdefault("NCCL_DEBUG", "WARN")
 
 CONFIGS = {
     # name: (N, D, V, ignore_fraction)  -- BASELINE.json configs
