@@ -4,8 +4,8 @@
 // reference simulates them in one process (per-shard kernel launches, rank-
 // ordered merge on the device); real multi-GPU runs use fce_vp_forward /
 // fce_vp_backward (include/fce/fce_vp.h) with one process per GPU.
-// SP gather and the DP step (parallel_sim.hpp:294-378) are not on the hot
-// path and are not provided.
+// SP gather and the DP step (parallel_sim.hpp:294-378) are provided with the
+// reference semantics on top of the same device path.
 #pragma once
 
 #include <span>
@@ -38,6 +38,15 @@ struct ShardLayout {
     }
     static ShardLayout tensor_parallel(std::size_t vocab, std::size_t ranks) {
         return make(ParallelMode::TensorParallel, vocab, ranks);
+    }
+    static ShardLayout sequence_parallel(std::size_t positions, std::size_t ranks) {
+        return make(ParallelMode::SequenceParallel, positions, ranks);
+    }
+    static ShardLayout data_parallel(std::size_t positions, std::size_t ranks) {
+        if (ranks != 0 && positions % ranks != 0)
+            throw InvalidLayout("data parallelism needs equal micro-batches: " + std::to_string(positions) +
+                                " positions across " + std::to_string(ranks) + " ranks");
+        return make(ParallelMode::DataParallel, positions, ranks);
     }
 };
 
@@ -219,6 +228,93 @@ TpGradients<T> tp_backward(const MatrixView<T>& hidden, const std::vector<Weight
         out.weight_shards.push_back(std::move(w));
     }
     if constexpr (std::is_same_v<T, float>) dh.download(out.hidden.data(), dh.bytes());
+    return out;
+}
+
+// ---------------------------------------------------------------- SP and DP
+// (reference parallel_sim.hpp:96-129 and 294-378)
+
+template <typename T>
+std::vector<MatrixView<T>> shard_positions(const MatrixView<T>& hidden, const ShardLayout& layout) {
+    if (layout.mode == ParallelMode::TensorParallel) throw InvalidLayout("position sharding requires an SP or DP layout");
+    if (layout.ranges.empty() || layout.ranges.back().hi != hidden.rows)
+        throw InvalidLayout("layout does not cover the positions");
+    std::vector<MatrixView<T>> out;
+    for (const ShardRange& r : layout.ranges) out.push_back(hidden.rows_slice(r.lo, r.hi));
+    return out;
+}
+
+inline std::vector<TargetVector> shard_targets(const TargetVector& targets, const ShardLayout& layout) {
+    if (layout.mode == ParallelMode::TensorParallel) throw InvalidLayout("target sharding requires an SP or DP layout");
+    if (layout.ranges.empty() || layout.ranges.back().hi != targets.size())
+        throw InvalidLayout("layout does not cover the positions");
+    std::vector<TargetVector> out;
+    for (const ShardRange& r : layout.ranges)
+        out.emplace_back(std::vector<std::int64_t>(targets.values().begin() + static_cast<std::ptrdiff_t>(r.lo),
+                                                   targets.values().begin() + static_cast<std::ptrdiff_t>(r.hi)),
+                         targets.ignore_index());
+    return out;
+}
+
+// SP -> TP switch: concatenate the position shards of H (host; on GPUs this is
+// an all-gather of H, paper_2511_17599_b200.vocab_parallel.sp_to_tp_gather).
+template <typename T>
+DenseMatrix<T> sp_to_tp_gather(const std::vector<MatrixView<T>>& shards) {
+    if (shards.empty()) throw InvalidLayout("no hidden shards to gather");
+    const std::size_t d = shards.front().cols;
+    std::size_t total = 0;
+    for (const auto& s : shards) {
+        if (s.cols != d) throw InvalidLayout("hidden shards disagree on width");
+        total += s.rows;
+    }
+    DenseMatrix<T> out(total, d);
+    std::size_t row = 0;
+    for (const auto& s : shards) {
+        std::copy(s.data, s.data + s.rows * s.cols, out.row(row));
+        row += s.rows;
+    }
+    return out;
+}
+
+template <typename T>
+struct DpReplica {
+    MatrixView<T> hidden;
+    TargetVector targets;
+};
+
+template <typename T>
+struct DpResult {
+    T loss = T{0};
+    DenseMatrix<T> weight_grad;
+};
+
+// Data-parallel step: every replica runs the fused forward + backward on its
+// micro-batch; loss and dW are averaged over replicas (the all-reduce-mean).
+template <typename T>
+DpResult<T> dp_step(const std::vector<DpReplica<T>>& replicas, const MatrixView<T>& weights, ReductionMode reduction,
+                    MemoryLedger& ledger, const ExecPolicy& policy = {}) {
+    if (replicas.empty()) throw InvalidLayout("no replicas");
+    if (reduction == ReductionMode::None) throw UnsupportedReduction("data-parallel loss sync requires a scalar reduction");
+    const std::size_t micro = replicas.front().hidden.rows;
+    for (const auto& r : replicas)
+        if (r.hidden.rows != micro || r.targets.size() != micro)
+            throw InvalidLayout("replica micro-batches must have equal sizes");
+    DpResult<T> out;
+    out.weight_grad = DenseMatrix<T>(weights.rows, weights.cols);
+    T loss_sum = T{0};
+    for (const auto& rep : replicas) {
+        FusedOutput<T> fwd = fused_forward(rep.hidden, weights, rep.targets, reduction, ledger, policy);
+        Gradients<T> g = fused_backward_recompute(rep.hidden, weights, rep.targets,
+                                                  std::span<const SoftmaxStats<T>>(fwd.stats),
+                                                  UpstreamGradient<T>::make_scalar(T{1}), reduction, ledger, policy);
+        loss_sum += fwd.loss.scalar();
+        T* acc = out.weight_grad.data();
+        const T* part = g.weights.data();
+        for (std::size_t i = 0; i < out.weight_grad.size(); ++i) acc[i] += part[i];
+    }
+    const T inv = T{1} / static_cast<T>(replicas.size());
+    out.loss = loss_sum * inv;
+    for (T& x : out.weight_grad.storage()) x *= inv;
     return out;
 }
 

@@ -169,3 +169,77 @@ class VocabParallel:
                                        reduction, upstream, ignore_index)
         dist.all_reduce(dh, group=self.group)
         return dh, dw
+
+
+# ------------------------------------------------------- SP -> TP and DP
+# (reference parallel_sim.hpp:294-378)
+
+def sp_to_tp_gather(hidden_shard, positions: int, group=None):
+    """Sequence-parallel -> tensor-parallel switch: every rank holds a ceil-first
+    position shard of H; all-gather them into the full H (sp_to_tp_gather,
+    parallel_sim.hpp:294-314).  Shards may be ragged (padded for the collective)."""
+    import torch
+    import torch.distributed as dist
+    world = dist.get_world_size(group)
+    ranges = fce.shard_ranges(positions, world)
+    rows = max(hi - lo for lo, hi in ranges)
+    pad = torch.zeros(rows, hidden_shard.shape[1], dtype=hidden_shard.dtype, device=hidden_shard.device)
+    pad[: hidden_shard.shape[0]] = hidden_shard
+    out = [torch.empty_like(pad) for _ in range(world)]
+    dist.all_gather(out, pad, group=group)
+    return torch.cat([o[: hi - lo] for o, (lo, hi) in zip(out, ranges)])
+
+
+def tp_to_sp_scatter(dhidden_partial, positions: int, group=None):
+    """Inverse of the gather for the backward: sum the ranks' dH partials and keep
+    this rank's position shard (a reduce-scatter; replaces the all-reduce when the
+    caller is sequence parallel)."""
+    import torch
+    import torch.distributed as dist
+    world, rank = dist.get_world_size(group), dist.get_rank(group)
+    ranges = fce.shard_ranges(positions, world)
+    rows = max(hi - lo for lo, hi in ranges)
+    parts = []
+    for lo, hi in ranges:
+        p = torch.zeros(rows, dhidden_partial.shape[1], dtype=dhidden_partial.dtype, device=dhidden_partial.device)
+        p[: hi - lo] = dhidden_partial[lo:hi]
+        parts.append(p)
+    out = torch.empty_like(parts[0])
+    if dist.get_backend(group) == "gloo":  # gloo has no reduce_scatter
+        full = torch.cat(parts)
+        dist.all_reduce(full, group=group)
+        out = full[rank * rows:(rank + 1) * rows].clone()
+    else:
+        dist.reduce_scatter(out, parts, group=group)
+    lo, hi = ranges[rank]
+    return out[: hi - lo]
+
+
+class LocalCompute:
+    """Per-replica fused forward + backward on this GPU (for dp_step)."""
+
+    def step(self, hidden, weight, targets, reduction, ignore_index):
+        out = fce.fused_forward(hidden, weight, targets, reduction, ignore_index)
+        dh, dw = fce.fused_backward_recompute(hidden, weight, targets, out.stats, reduction, 1.0, ignore_index)
+        return out.loss, dh, dw
+
+
+def dp_step(hidden, weight, targets, reduction="mean", ignore_index=None, group=None, compute=None):
+    """Data-parallel step (dp_step, parallel_sim.hpp:334-378): every rank runs the
+    fused forward + backward on its micro-batch; loss and dW are averaged over
+    ranks with all-reduce; dH stays rank-local.  Returns (loss, dH, dW)."""
+    import torch
+    import torch.distributed as dist
+    if reduction == "none":
+        raise fce.UnsupportedReduction("data-parallel loss sync requires a scalar reduction")
+    world = dist.get_world_size(group)
+    sizes = [torch.zeros(1, dtype=torch.int64) for _ in range(world)]
+    dist.all_gather(sizes, torch.tensor([hidden.shape[0]], dtype=torch.int64), group=group) \
+        if dist.get_backend(group) == "gloo" else None
+    if dist.get_backend(group) == "gloo" and len({int(s) for s in sizes}) != 1:
+        raise fce.InvalidLayout("replica micro-batches must have equal sizes")
+    loss, dh, dw = (compute or LocalCompute()).step(hidden, weight, targets, reduction, ignore_index)
+    loss = torch.as_tensor(loss, dtype=torch.float32, device=dw.device).reshape(1).clone()
+    dist.all_reduce(loss, group=group)
+    dist.all_reduce(dw, group=group)
+    return loss / world, dh, dw / world

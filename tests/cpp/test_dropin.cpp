@@ -193,6 +193,31 @@ static void test_tp_matches_single() {
     CHECK(s.target_found == part.stats[3].target_found);
 }
 
+static void test_sp_dp() {
+    // SP round trip (test_parallel_sim.cpp:240-252) and DP equivalence (271-298)
+    Instance<float> inst = instance(48, 16, 200, 9, 0.0);
+    MemoryLedger ledger;
+    MatrixView<float> hv(inst.hidden), wv(inst.weights);
+    auto sp = shard_positions(hv, ShardLayout::sequence_parallel(48, 3));
+    DenseMatrix<float> back = sp_to_tp_gather(sp);
+    CHECK(back.storage() == inst.hidden.storage());
+    auto layout = ShardLayout::data_parallel(48, 4);
+    auto hs = shard_positions(hv, layout);
+    auto ts = shard_targets(inst.targets, layout);
+    std::vector<DpReplica<float>> reps;
+    for (std::size_t r = 0; r < 4; ++r) reps.push_back(DpReplica<float>{hs[r], ts[r]});
+    DpResult<float> dp = dp_step(reps, wv, ReductionMode::Mean, ledger);
+    // equal micro-batches with mean reduction: DP mean == global mean
+    auto full = fused_forward(hv, wv, inst.targets, ReductionMode::Mean, ledger);
+    CHECK(std::fabs(dp.loss - full.loss.scalar()) < 1e-5);
+    auto g = fused_backward_recompute(hv, wv, inst.targets, std::span<const SoftmaxStats<float>>(full.stats),
+                                      UpstreamGradient<float>::make_scalar(1.f), ReductionMode::Mean, ledger);
+    CHECK(relmax(dp.weight_grad.data(), g.weights.data(), g.weights.size()) < 1e-2);
+    CHECK(throws_as<InvalidLayout>([&] { ShardLayout::data_parallel(10, 4); }));
+    CHECK(throws_as<UnsupportedReduction>([&] { dp_step(reps, wv, ReductionMode::None, ledger); }));
+    CHECK(ledger.current_bytes() == 0);
+}
+
 int main() {
     std::printf("drop-in C++ API tests\n");
     test_worked_example();
@@ -202,6 +227,7 @@ int main() {
     test_two_class_hand_example();
     test_errors();
     test_tp_matches_single();
+    test_sp_dp();
     std::printf("%d checks, %d failed\n", g_checks, g_fail);
     return g_fail ? 1 : 0;
 }

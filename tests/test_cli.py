@@ -1,0 +1,43 @@
+"""The fusedce-style CLI (reference tests/test_cli.cpp): exit codes, verify
+suites, bench CSV schema (bench.cpp:200-211)."""
+import os
+import subprocess
+import sys
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def run(*args):
+    return subprocess.run([sys.executable, "-m", "paper_2511_17599_b200.cli", *args], cwd=ROOT,
+                          capture_output=True, text=True, timeout=600)
+
+
+def test_usage_errors_exit_2():
+    assert run().returncode == 2
+    assert run("bench", "--methods", "bogus").returncode == 2
+    assert run("--help").returncode == 0
+
+
+@pytest.mark.gpu
+def test_verify_passes(cuda):
+    r = run("verify", "--loss-instances", "12", "--grad-instances", "4")
+    assert r.returncode == 0, r.stdout + r.stderr
+    for suite in ("loss_equivalence", "gradient_recompute", "window_sweep", "shard_invariance", "stability"):
+        assert suite in r.stdout
+    assert "overall: PASS" in r.stdout
+
+
+@pytest.mark.gpu
+def test_bench_csv_schema(cuda, tmp_path):
+    out = tmp_path / "b.csv"
+    r = run("bench", "--bt", "256", "--vocab", "2048", "--hidden", "128", "--repeats", "2", "--warmup", "1",
+            "--methods", "canonical,fused,fused_windowed,fused_partial_grad", "--window", "512",
+            "--output", str(out))
+    assert r.returncode == 0, r.stderr
+    lines = out.read_text().strip().splitlines()
+    assert lines[0] == "bt,vocab,hidden,method,precision,latency_s,latency_min_s,latency_max_s,aux_peak_bytes,loss"
+    assert len(lines) == 5 and all(len(l.split(",")) == 10 for l in lines)
+    losses = [float(l.split(",")[9]) for l in lines[1:]]
+    assert max(losses) - min(losses) < 1e-3 * abs(losses[0])  # every method computes the same loss
