@@ -447,13 +447,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(128 + 32 * kEpiWarps
                     if (un.type == kUnitGrad) {
                         const bool row_ok = lrow < un.nc;
                         const int64_t grow = static_cast<int64_t>(un.r0) + lrow;
-                        float gam = 0.f, l2lse = 0.f;
+                        float gam = 0.f, lse_r = 0.f;
                         int64_t tcol = -1;
                         if (row_ok) {
                             const int64_t y = p.targets[grow];
                             const bool skip = p.has_ignore && y == p.ignore_index;
                             gam = skip ? 0.f : p.gamma[grow];
-                            l2lse = skip ? 0.f : p.lse[grow] * kL2e;
+                            lse_r = skip ? 0.f : p.lse[grow];
                             tcol = y - (p.v_offset + un.vb);
                         }
 #pragma unroll 1
@@ -470,8 +470,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(128 + 32 * kEpiWarps
                                 const int64_t tc = tcol - col0;
 #pragma unroll
                                 for (int j = 0; j < 32; j += 2) {
-                                    float g0 = gam * (ex2(fmaf(v[j], kL2e, -l2lse)) - (tc == j ? 1.f : 0.f));
-                                    float g1 = gam * (ex2(fmaf(v[j + 1], kL2e, -l2lse)) - (tc == j + 1 ? 1.f : 0.f));
+                                    float g0 = gam * (ex2((v[j] - lse_r) * kL2e) - (tc == j ? 1.f : 0.f));
+                                    float g1 = gam * (ex2((v[j + 1] - lse_r) * kL2e) - (tc == j + 1 ? 1.f : 0.f));
                                     if (gam == 0.f || col0 + j >= un.vc) g0 = 0.f;
                                     if (gam == 0.f || col0 + j + 1 >= un.vc) g1 = 0.f;
                                     packed[h2 * 16 + (j >> 1)] = pack_bf16(g0, g1);
@@ -524,13 +524,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(128 + 32 * kEpiWarps
                 } else if (un.type == kUnitGrad) {
                     const bool row_ok = lrow < un.nc;
                     const int64_t grow = static_cast<int64_t>(un.r0) + lrow;
-                    float gam = 0.f, l2lse = 0.f;
+                    float gam = 0.f, lse_r = 0.f;
                     int64_t tcol = -1;
                     if (row_ok) {
                         const int64_t y = p.targets[grow];
                         const bool skip = p.has_ignore && y == p.ignore_index;
                         gam = skip ? 0.f : p.gamma[grow];
-                        l2lse = skip ? 0.f : p.lse[grow] * kL2e;
+                        lse_r = skip ? 0.f : p.lse[grow];
                         tcol = y - (p.v_offset + un.vb);
                     }
                     __nv_bfloat16* grow_ptr =
@@ -546,8 +546,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(128 + 32 * kEpiWarps
                             uint32_t packed[16];
 #pragma unroll
                             for (int j = 0; j < 32; j += 2) {
-                                float g0 = gam * (ex2(fmaf(v[j], kL2e, -l2lse)) - (tc == j ? 1.f : 0.f));
-                                float g1 = gam * (ex2(fmaf(v[j + 1], kL2e, -l2lse)) - (tc == j + 1 ? 1.f : 0.f));
+                                float g0 = gam * (ex2((v[j] - lse_r) * kL2e) - (tc == j ? 1.f : 0.f));
+                                float g1 = gam * (ex2((v[j + 1] - lse_r) * kL2e) - (tc == j + 1 ? 1.f : 0.f));
                                 if (gam == 0.f || col0 + j >= un.vc) g0 = 0.f;
                                 if (gam == 0.f || col0 + j + 1 >= un.vc) g1 = 0.f;
                                 packed[j >> 1] = pack_bf16(g0, g1);

@@ -235,7 +235,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             int64_t tcol = -1;  // launch-local column of this row's target
             float m_run = -INFINITY, a_run = 0.f, zt = 0.f;
             bool found = false;
-            float l2lse = 0.f, gam = 0.f;
+            float lse_r = 0.f, gam = 0.f;
             if (EPI != kEpiGemm) {
                 row_ok = row < p.n_rows;
                 if (row_ok) {
@@ -244,7 +244,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                     tcol = y - p.col_global0;
                     if (EPI == kEpiGrad) {
                         gam = skip ? 0.f : p.gamma[row];
-                        l2lse = skip ? 0.f : p.lse[row] * kLog2e;
+                        lse_r = skip ? 0.f : p.lse[row];
                     }
                 }
             }
@@ -274,12 +274,11 @@ __global__ void __launch_bounds__(kThreads, 1)
                             m_run = cmax;
                         }
                         if (cmax != -INFINITY) {
-                            const float mb = m_run * kLog2e;
                             float s0 = 0.f, s1 = 0.f;
 #pragma unroll
                             for (int j = 0; j < 32; j += 2) {
-                                s0 += ex2(fmaf(v[j], kLog2e, -mb));
-                                s1 += ex2(fmaf(v[j + 1], kLog2e, -mb));
+                                s0 += ex2((v[j] - m_run) * kLog2e);
+                                s1 += ex2((v[j + 1] - m_run) * kLog2e);
                             }
                             a_run += s0 + s1;
                         }
@@ -298,9 +297,9 @@ __global__ void __launch_bounds__(kThreads, 1)
                             uint32_t packed[16];
 #pragma unroll
                             for (int j = 0; j < 32; j += 2) {
-                                float g0 = gam * (ex2(fmaf(v[j], kLog2e, -l2lse)) -
+                                float g0 = gam * (ex2((v[j] - lse_r) * kLog2e) -
                                                   (tc == j ? 1.f : 0.f));
-                                float g1 = gam * (ex2(fmaf(v[j + 1], kLog2e, -l2lse)) -
+                                float g1 = gam * (ex2((v[j + 1] - lse_r) * kLog2e) -
                                                   (tc == j + 1 ? 1.f : 0.f));
                                 if (gam == 0.f || col0 + j >= p.v_cols) g0 = 0.f;
                                 if (gam == 0.f || col0 + j + 1 >= p.v_cols) g1 = 0.f;
