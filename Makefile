@@ -26,9 +26,9 @@ $(DROPIN_TEST): tests/cpp/test_dropin.cpp $(wildcard include/fusedce/*.hpp inclu
 	    -L$(PKG) -lfce -Loracle -loracle -L/usr/local/cuda/lib64 -lcudart \
 	    -Wl,-rpath,'$$ORIGIN/../../$(PKG)' -Wl,-rpath,'$$ORIGIN/../../oracle' -Wl,-rpath,/usr/local/cuda/lib64
 
-$(LIB): $(CSRC)/fce_kernels.cu $(CSRC)/fce_bwd.cu $(CSRC)/fce_pair.cu $(CSRC)/fce_api.cpp $(CSRC)/fce_vp.cpp $(CSRC)/fce_internal.h \
+$(LIB): $(CSRC)/fce_kernels.cu $(CSRC)/fce_bwd.cu $(CSRC)/fce_pair.cu $(CSRC)/fce_fwd_pair.cu $(CSRC)/fce_api.cpp $(CSRC)/fce_vp.cpp $(CSRC)/fce_internal.h \
         $(CSRC)/sm100_ptx.cuh include/fce/fce.h
-	$(NVCC) $(NVFLAGS) -shared -cudart static -o $@ $(CSRC)/fce_kernels.cu $(CSRC)/fce_bwd.cu $(CSRC)/fce_pair.cu $(CSRC)/fce_api.cpp \
+	$(NVCC) $(NVFLAGS) -shared -cudart static -o $@ $(CSRC)/fce_kernels.cu $(CSRC)/fce_bwd.cu $(CSRC)/fce_pair.cu $(CSRC)/fce_fwd_pair.cu $(CSRC)/fce_api.cpp \
 	    $(CSRC)/fce_vp.cpp -ldl -lpthread -lrt
 
 $(ORACLE): oracle/fce_oracle.c oracle/fce_oracle.h

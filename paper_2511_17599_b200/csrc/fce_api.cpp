@@ -55,10 +55,12 @@ struct fce_handle_s {
     int64_t splits = 0, band_cols = 0, row_chunk = 0, validate = 1, bwd_persistent = 1;
     int64_t l2_hints = 1;
     int64_t gemm_pair = 1;
+    int64_t fwd_pair = 0;     // forward on CTA pairs (fce_fwd_pair.cu); measured slower under the power cap
     int64_t bwd_unit_mask = 7;
     int64_t trace_ptr = 0;
     int64_t bwd_epi_warps = 8;
-    int64_t bwd_tma_epi = 1;  // dev only: device buffer for per-unit timestamps
+    int64_t bwd_tma_epi = 1;
+    int64_t dh_group = 1;     // bands per dH group in the persistent backward  // dev only: device buffer for per-unit timestamps
     int64_t launches = 0;
     size_t bwd_scratch[4] = {0, 0, 0, 0};  // offsets of the persistent-backward scratch
     // optional per-kernel CUDA-event timing of the tile kernels (bench roofline)
@@ -208,14 +210,16 @@ cudaEvent_t pool_event(fce_handle h) {
 
 // Launches one tile kernel; with timing on, brackets it with CUDA events on
 // the handle's stream and records its algorithmic flop count.
-cudaError_t timed_launch(fce_handle h, const TileParams& p, const TensorMaps& maps, double flops) {
+cudaError_t timed_launch(fce_handle h, const TileParams& p, const TensorMaps& maps, double flops,
+                         bool fwd_pair = false) {
     cudaEvent_t e0 = nullptr, e1 = nullptr;
     if (h->timing) {
         e0 = pool_event(h);
         e1 = pool_event(h);
         cudaEventRecord(e0, h->stream);
     }
-    cudaError_t e = launch_tile_kernel(p, maps, h->sms, h->stream);
+    cudaError_t e = fwd_pair ? launch_fwd_pair(p, maps, h->sms, h->stream)
+                             : launch_tile_kernel(p, maps, h->sms, h->stream);
     if (h->timing) {
         cudaEventRecord(e1, h->stream);
         h->pending.push_back({p.mode, e0, e1, flops});
@@ -238,22 +242,42 @@ void drain_timing(fce_handle h) {
     h->pending.clear();
 }
 
-fce_status run_forward_tiles(fce_handle h, const fce_problem* p, int splits, float* pm, float* pa,
+// Forward geometry: row blocks of 256 (CTA pairs) or 128 rows, and the
+// split-V factor over the persistent grid (pairs count as one slot each).
+struct FwdGeom {
+    bool pair;
+    int64_t m_blocks, v_tiles;
+    int splits;
+};
+
+FwdGeom forward_geometry(fce_handle h, const fce_problem* p, int64_t window) {
+    FwdGeom g;
+    g.pair = h->fwd_pair != 0;
+    g.m_blocks = ceil_div(p->n, g.pair ? 256 : kBM);
+    g.v_tiles = ceil_div(p->v, kBN);
+    g.splits = choose_splits(g.m_blocks, g.v_tiles, g.pair ? h->sms / 2 : h->sms, h->splits);
+    if (window > 0) g.splits = static_cast<int>(std::min<int64_t>(g.v_tiles, ceil_div(p->v, window)));
+    return g;
+}
+
+fce_status run_forward_tiles(fce_handle h, const fce_problem* p, const FwdGeom& g, float* pm, float* pa,
                              float* pzt, uint8_t* pf) {
     TileParams tp;
     std::memset(&tp, 0, sizeof(tp));
     TensorMaps maps;
     std::memset(&maps, 0, sizeof(maps));
+    // pair: each CTA stages its 128 rows of H and its 128-row half of the W tile
+    const uint32_t b_box = g.pair ? 128 : kBN;
     if (!encode_map_2d(&maps.a0, p->hidden, p->d, p->n, p->ldh * 2, kBK, kBM) ||
-        !encode_map_2d(&maps.b0, p->weight, p->d, p->v, p->ldw * 2, kBK, kBN))
+        !encode_map_2d(&maps.b0, p->weight, p->d, p->v, p->ldw * 2, kBK, b_box))
         return fail(FCE_CUDA_ERROR, "cuTensorMapEncodeTiled failed for H / W");
     tp.mode = kEpiForward;
     tp.n_rows = static_cast<int>(p->n);
     tp.v_cols = static_cast<int>(p->v);
-    tp.m_blocks = static_cast<int>(ceil_div(p->n, kBM));
-    tp.v_tiles = static_cast<int>(ceil_div(p->v, kBN));
-    tp.splits = splits;
-    tp.m_group = std::min(tp.m_blocks, 16);
+    tp.m_blocks = static_cast<int>(g.m_blocks);
+    tp.v_tiles = static_cast<int>(g.v_tiles);
+    tp.splits = g.splits;
+    tp.m_group = std::min(tp.m_blocks, g.pair ? 8 : 16);
     tp.k_blocks = static_cast<int>(ceil_div(p->d, kBK));
     tp.units = tp.m_blocks * tp.splits;
     tp.targets = p->targets;
@@ -264,7 +288,7 @@ fce_status run_forward_tiles(fce_handle h, const fce_problem* p, int splits, flo
     tp.part_a = pa;
     tp.part_zt = pzt;
     tp.part_found = pf;
-    cudaError_t e = timed_launch(h, tp, maps, 2.0 * p->n * p->d * p->v);
+    cudaError_t e = timed_launch(h, tp, maps, 2.0 * p->n * p->d * p->v, g.pair);
     if (e != cudaSuccess) return fail(FCE_CUDA_ERROR, "forward tile kernel: %s", cudaGetErrorString(e));
     return FCE_OK;
 }
@@ -272,7 +296,7 @@ fce_status run_forward_tiles(fce_handle h, const fce_problem* p, int splits, flo
 // Persistent backward: one launch of fce_bwd_persistent_kernel over every
 // (row chunk x vocab band) chunk; see fce_bwd.cu for the schedule.
 fce_status run_backward_persistent(fce_handle h, const fce_problem* p, const float* gamma,
-                                   const float* lse, int64_t row_chunk, int64_t band,
+                                   const float* lse, int64_t row_chunk, int64_t band, int kg,
                                    float* dhidden, int64_t lddh, float* dweight, int64_t lddw,
                                    int accumulate_dhidden) {
     char* ws = static_cast<char*>(h->ws);
@@ -292,10 +316,14 @@ fce_status run_backward_persistent(fce_handle h, const fce_problem* p, const flo
     bp.n_g = mb_max * bp.vt;
     bp.n_dh = dhidden ? mb_max * d_tiles : 0;
     bp.n_dw = dweight ? bp.vm * d_tiles : 0;
-    bp.per_chunk = bp.n_g + bp.n_dh + bp.n_dw;
-    const int64_t units = n_chunks * bp.per_chunk;
+    bp.kg = kg;
+    bp.gpr = static_cast<int>(ceil_div(n_bd, kg));
+    bp.per_gf = kg * (bp.n_g + bp.n_dw) + bp.n_dh;
+    const int64_t per_rc = n_bd * (bp.n_g + bp.n_dw) + bp.gpr * bp.n_dh;
+    const int64_t units = n_rc * per_rc;
     if (units >= INT32_MAX) return fail(FCE_INVALID_LAYOUT, "too many backward work units");
     bp.units = static_cast<int>(units);
+    bp.per_rc = static_cast<int>(per_rc);
     bp.d_tiles = d_tiles;
     bp.k_blocks_d = static_cast<int>(ceil_div(p->d, kBK));
     bp.mb_max = mb_max;
@@ -310,6 +338,7 @@ fce_status run_backward_persistent(fce_handle h, const fce_problem* p, const flo
     bp.trace = reinterpret_cast<unsigned long long*>(h->trace_ptr);
     bp.nc_max = row_chunk;
     bp.ldg = band;
+    bp.ldr = band * kg;
     bp.d = p->d;
     bp.lddh = lddh;
     bp.lddw = lddw;
@@ -324,9 +353,14 @@ fce_status run_backward_persistent(fce_handle h, const fce_problem* p, const flo
     bp.dw = dweight;
 
     FCE_CUDA(cudaMemsetAsync(d_ctr, 0, sizeof(unsigned) * (1 + 4 * n_chunks + n_chunks * mb_max), h->stream));
-    // stale ring rows past a short last chunk are read (then masked or
-    // multiplied by zero-filled operands): keep them finite
-    FCE_CUDA(cudaMemsetAsync(g_ring, 0, sizeof(__nv_bfloat16) * 2 * row_chunk * band, h->stream));
+    // ring rows past a short last row chunk (up to its 256-row unit edge) are
+    // read by dW units and multiplied by zero-filled H rows: keep them finite
+    const int64_t nc_last = p->n - (n_rc - 1) * row_chunk;
+    const int64_t tail = std::min(round_up(nc_last, 256), row_chunk) - nc_last;
+    if (tail > 0)
+        for (int s2 = 0; s2 < 2; ++s2)
+            FCE_CUDA(cudaMemsetAsync(g_ring + (s2 * row_chunk + nc_last) * bp.ldr, 0,
+                                     sizeof(__nv_bfloat16) * tail * bp.ldr, h->stream));
 
     BwdMaps maps;
     std::memset(&maps, 0, sizeof(maps));
@@ -334,9 +368,9 @@ fce_status run_backward_persistent(fce_handle h, const fce_problem* p, const flo
     // pair units: every CTA loads 128 rows of K-major operands per stage
     if (!encode_map_2d(&maps.h_k, p->hidden, p->d, p->n, p->ldh * 2, kBK, 128) ||
         !encode_map_2d(&maps.w_k, p->weight, p->d, p->v, p->ldw * 2, kBK, 128) ||
-        !encode_map_2d(&maps.g_k, g_ring, band, ring_rows, band * 2, kBK, 128) ||
+        !encode_map_2d(&maps.g_k, g_ring, bp.ldr, ring_rows, bp.ldr * 2, kBK, 128) ||
         !encode_map_2d(&maps.w_mn, p->weight, p->d, p->v, p->ldw * 2, 64, 64) ||
-        !encode_map_2d(&maps.g_mn, g_ring, band, ring_rows, band * 2, 64, 64) ||
+        !encode_map_2d(&maps.g_mn, g_ring, bp.ldr, ring_rows, bp.ldr * 2, 64, 64) ||
         !encode_map_2d(&maps.h_mn, p->hidden, p->d, p->n, p->ldh * 2, 64, 64))
         return fail(FCE_CUDA_ERROR, "cuTensorMapEncodeTiled failed (persistent backward)");
 
@@ -344,7 +378,7 @@ fce_status run_backward_persistent(fce_handle h, const fce_problem* p, const flo
     // TMA (16-byte aligned rows); otherwise per-thread vector stores
     bp.tma_epi = 0;
     if (h->bwd_tma_epi) {
-        bool ok = encode_map_2d(&maps.g_st, g_ring, band, ring_rows, band * 2, 64, 128);
+        bool ok = encode_map_2d(&maps.g_st, g_ring, bp.ldr, ring_rows, bp.ldr * 2, 64, 128);
         if (ok && dhidden) ok = encode_map_2d(&maps.dh_st, dhidden, p->d, p->n, lddh * 4, 32, 128, true);
         if (ok && dweight) ok = encode_map_2d(&maps.dw_st, dweight, p->d, p->v, lddw * 4, 32, 128, true);
         bp.tma_epi = ok ? 1 : 0;
@@ -468,7 +502,12 @@ fce_status fce_set_option(fce_handle h, const char* key, int64_t value) {
     } else if (!std::strcmp(key, "trace_ptr")) {
         h->trace_ptr = value;
     } else if (!std::strcmp(key, "bwd_unit_mask")) {
-        h->bwd_unit_mask = value & 63;
+        h->bwd_unit_mask = value & 255;
+    } else if (!std::strcmp(key, "dh_group")) {
+        if (value < 1 || value > 64) return fail(FCE_INVALID_ARGUMENT, "dh_group must be in [1, 64]");
+        h->dh_group = value;
+    } else if (!std::strcmp(key, "fwd_pair")) {
+        h->fwd_pair = value ? 1 : 0;
     } else if (!std::strcmp(key, "gemm_pair")) {
         h->gemm_pair = value ? 1 : 0;
     } else if (!std::strcmp(key, "l2_hints")) {
@@ -524,9 +563,8 @@ fce_status fce_forward(fce_handle h, const fce_problem* p, int reduction, int64_
     h->launches += 1;
     if ((s = read_errors(h, h->validate != 0))) return s;
 
-    const int64_t m_blocks = ceil_div(p->n, kBM), v_tiles = ceil_div(p->v, kBN);
-    int splits = choose_splits(m_blocks, v_tiles, h->sms, h->splits);
-    if (window > 0) splits = static_cast<int>(std::min<int64_t>(v_tiles, ceil_div(p->v, window)));
+    const FwdGeom geom = forward_geometry(h, p, window);
+    const int splits = geom.splits;
 
     Scratch sc(h);
     const size_t o_m = sc.take(sizeof(float) * splits * p->n);
@@ -536,7 +574,7 @@ fce_status fce_forward(fce_handle h, const fce_problem* p, int reduction, int64_
     const size_t o_b = sc.take(sizeof(double) * (ceil_div(p->n, 256) + 1));
     if ((s = sc.commit())) return s;
 
-    if ((s = run_forward_tiles(h, p, splits, sc.ptr<float>(o_m), sc.ptr<float>(o_a),
+    if ((s = run_forward_tiles(h, p, geom, sc.ptr<float>(o_m), sc.ptr<float>(o_a),
                                sc.ptr<float>(o_z), sc.ptr<uint8_t>(o_f))))
         return s;
     int blocks = 0;
@@ -565,15 +603,15 @@ fce_status fce_forward_partial(fce_handle h, const fce_problem* p, fce_stats par
     if (e != cudaSuccess) return fail(FCE_CUDA_ERROR, "prep kernel: %s", cudaGetErrorString(e));
     h->launches += 1;
     if ((s = read_errors(h, h->validate != 0))) return s;
-    const int64_t m_blocks = ceil_div(p->n, kBM), v_tiles = ceil_div(p->v, kBN);
-    const int splits = choose_splits(m_blocks, v_tiles, h->sms, h->splits);
+    const FwdGeom geom = forward_geometry(h, p, 0);
+    const int splits = geom.splits;
     Scratch sc(h);
     const size_t o_m = sc.take(sizeof(float) * splits * p->n);
     const size_t o_a = sc.take(sizeof(float) * splits * p->n);
     const size_t o_z = sc.take(sizeof(float) * splits * p->n);
     const size_t o_f = sc.take(splits * p->n);
     if ((s = sc.commit())) return s;
-    if ((s = run_forward_tiles(h, p, splits, sc.ptr<float>(o_m), sc.ptr<float>(o_a),
+    if ((s = run_forward_tiles(h, p, geom, sc.ptr<float>(o_m), sc.ptr<float>(o_a),
                                sc.ptr<float>(o_z), sc.ptr<uint8_t>(o_f))))
         return s;
     e = launch_merge_stats(splits, p->n, p->n, sc.ptr<float>(o_m), sc.ptr<float>(o_a),
@@ -649,11 +687,14 @@ fce_status fce_backward(fce_handle h, const fce_problem* p, fce_stats stats, int
                                  : std::max<int64_t>(kBN, ((int64_t(16) << 20) / row_chunk) / kBN * kBN);
     }
     band = std::min(band, round_up(p->v, kBN));
+    // bands per dH group (persistent backward): dH is written once per group
+    const int64_t n_bd_all = ceil_div(p->v, band);
+    const int kg = h->bwd_persistent ? static_cast<int>(std::min<int64_t>(h->dh_group, n_bd_all)) : 1;
 
     Scratch sc(h);
     const size_t o_g = sc.take(sizeof(float) * p->n);
     const size_t o_l = sc.take(sizeof(float) * p->n);
-    const size_t o_G = sc.take(sizeof(__nv_bfloat16) * row_chunk * band * (h->bwd_persistent ? 2 : 1));
+    const size_t o_G = sc.take(sizeof(__nv_bfloat16) * row_chunk * band * (h->bwd_persistent ? 2 * kg : 1));
     const int64_t n_rc = ceil_div(p->n, row_chunk), n_bd = ceil_div(p->v, band);
     const int64_t n_chunks = n_rc * n_bd;
     const int64_t mb_max = ceil_div(row_chunk, 128);
@@ -680,7 +721,7 @@ fce_status fce_backward(fce_handle h, const fce_problem* p, fce_stats stats, int
     if (!dhidden && !dweight) return FCE_OK;
 
     if (h->bwd_persistent)
-        return run_backward_persistent(h, p, gamma, lse, row_chunk, band, dhidden, lddh, dweight,
+        return run_backward_persistent(h, p, gamma, lse, row_chunk, band, kg, dhidden, lddh, dweight,
                                        lddw, accumulate_dhidden);
 
     const int k_blocks_d = static_cast<int>(ceil_div(p->d, kBK));

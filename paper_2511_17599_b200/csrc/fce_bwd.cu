@@ -6,30 +6,40 @@
 // pairs: S = H.W^T (recompute, contract d), dH = G.W (contract v) and
 // dW = G^T.H (contract n).  At D = 4096 neither dH[m,:] nor dW[v,:] fits TMEM,
 // so each contraction stays output-stationary on the tensor cores and only
-// G = gamma (softmax - onehot), bf16, moves between them through a 2-slot ring
-// of (row chunk x vocab band) chunks sized to stay L2-resident.
+// G = gamma (softmax - onehot), bf16, moves between them through a ring of
+// two group slots in HBM.
 //
 // Execution: CTA pairs (cluster of 2, tcgen05.mma.cta_group::2, M = 256): each
 // CTA loads its 128 rows of A and its 128 columns of B per 64-deep K stage
 // (32 KB, 6 stages), the even CTA issues the MMAs for both, and each CTA's
 // epilogue drains its own 128 accumulator rows.  A unit is a 256 x 256 tile.
+//
+// Geometry: rows are cut into row chunks (nc_max rows), the vocabulary into
+// bands (ldg columns); chunk c = (row chunk, band).  The bands of a row chunk
+// form dH groups of kg consecutive bands: dH = G . W contracts a whole group
+// (K = kg * band) before it is written, so the fp32 dH read-modify-write
+// traffic (N x D x 4 B per write, the dominant HBM stream of the backward)
+// drops kg-fold.  A group's G lives in ring slot (group & 1), band j of the
+// group at columns [j * band, (j + 1) * band).
+//
 // Work units of one launch, dispatched in this order by an atomic counter
-// (work stealing per pair):
-//     G(0) M(0) G(1) M(1) ... G(C-1) M(C-1)
-//   G(c): 256x256 S tiles of chunk c -> G tile into ring slot c % 2
-//   M(c): dH units (256 rows x 256 d, K = band) then dW units (256 vocab rows
-//         x 256 d, K = row chunk) reading ring slot c % 2
-// Every chunk is counted at full (row_chunk x band) geometry so a unit index
-// decodes with two divisions; units that fall past N or V in the last row
-// chunk / band are empty (no loads, no MMA) but still signal completion.
-// Dependencies (waited by the TMA producer before it loads a unit, released by
+// (work stealing per pair); per group with chunks c0 .. c(nb-1):
+//     G(c0)  G(c1) dW(c0)  G(c2) dW(c1) ...  G(c(nb-1))  dH(group)  dW(c(nb-1))
+//   G(c):  256x256 S tiles of chunk c -> G tile into the group's ring slot
+//   dW(c): 256 vocab rows x 256 d, K = row chunk, reading band c's G columns
+//   dH(g): 256 rows x 256 d, K = the group's vocabulary
+// (dW lags its G by one band so a dW unit rarely waits for G stragglers; with
+// kg = 1 the order is G(c) dH(c) dW(c).)  Every chunk is counted at full
+// (row_chunk x band) geometry so a unit index decodes in closed form; units
+// that fall past N or V are empty (no loads, no MMA) but still signal.
+// Dependencies (waited by the scheduler before it publishes a unit, released by
 // the epilogue with a gpu-scope fence + atomic; every wait targets a unit
 // dispatched earlier, so the schedule cannot deadlock):
-//   G(c)        needs M(c-2) complete            (ring slot reuse)
-//   dH(c, mb)   needs G(c) rows of mb complete   and dH(c-1) complete when c
-//               is not the first band of its row chunk (fixed fp32 add order)
-//   dW(c)       needs G(c) complete              and dW(c - bands) complete when
-//               c is not in the first row chunk (store, then ordered adds)
+//   G(c)       needs every dH / dW unit of group(c) - 2 complete (slot reuse)
+//   dH(g, mb)  needs the G rows of mb in every chunk of g, and dH(g - 1) when g
+//              is not the first group of its row chunk (fixed fp32 add order)
+//   dW(c)      needs G(c) complete, and dW(c - bands) when c is not in the
+//              first row chunk (store, then ordered adds)
 #include <cmath>
 #include <cstdio>
 
@@ -54,15 +64,18 @@ enum UnitType : int { kUnitGrad = 0, kUnitDH = 1, kUnitDW = 2, kUnitStop = 3 };
 
 struct BUnit {
     int type;     // UnitType
-    int c;        // chunk
+    int c;        // chunk (grad, dW); last chunk of the group (dH)
     int m_blk;    // 256-row block: chunk rows (grad, dH) or band vocab rows (dW)
     int n_tile;   // 256-wide tile: band vocab (grad) or d (dH, dW)
     int r0, nc;   // chunk rows [r0, r0 + nc)
-    int vb, vc;   // band vocab rows [vb, vb + vc)
-    int slot, row_idx, band_idx;
+    int vb, vc;   // vocab rows [vb, vb + vc): the band (grad, dW) or the group (dH)
+    int slot;     // ring slot of the group
+    int gcol;     // ring column of this band's G (grad, dW)
+    int row_idx, gl, c0, nb;  // row chunk, group within it, its first chunk, bands
     bool empty;   // past N or V: no loads / MMA / stores, completion only
 };
 
+// Closed-form decode of the dispatch order described at the top of the file.
 __device__ __forceinline__ BUnit decode_unit(const BwdParams& p, int u) {
     BUnit r;
     if (u >= p.units) {
@@ -70,33 +83,62 @@ __device__ __forceinline__ BUnit decode_unit(const BwdParams& p, int u) {
         r.empty = true;
         return r;
     }
-    const int c = u / p.per_chunk;
-    const int l = u - c * p.per_chunk;
-    r.c = c;
-    r.row_idx = c / p.bands;
-    r.band_idx = c - r.row_idx * p.bands;
-    r.slot = c & 1;
-    r.r0 = r.row_idx * static_cast<int>(p.nc_max);
-    r.nc = min(static_cast<int>(p.nc_max), p.n - r.r0);
-    r.vb = r.band_idx * static_cast<int>(p.ldg);
-    r.vc = min(static_cast<int>(p.ldg), p.v - r.vb);
+    r.row_idx = u / p.per_rc;
+    const int lu = u - r.row_idx * p.per_rc;
+    r.gl = min(lu / p.per_gf, p.gpr - 1);
+    int l = lu - r.gl * p.per_gf;
+    r.nb = min(p.kg, p.bands - r.gl * p.kg);
+    r.c0 = r.row_idx * p.bands + r.gl * p.kg;
+    r.slot = (r.row_idx * p.gpr + r.gl) & 1;
+    const int blk = p.n_g + p.n_dw;
+    int j, loc;
     if (l < p.n_g) {
         r.type = kUnitGrad;
-        r.m_blk = l / p.vt;
-        r.n_tile = l - r.m_blk * p.vt;
-        r.empty = r.m_blk * kPM >= r.nc || r.n_tile * kBN >= r.vc;
-    } else if (l < p.n_g + p.n_dh) {
-        const int l2 = l - p.n_g;
-        r.type = kUnitDH;
-        r.m_blk = l2 / p.d_tiles;
-        r.n_tile = l2 - r.m_blk * p.d_tiles;
+        j = 0;
+        loc = l;
+    } else if ((l -= p.n_g) < (r.nb - 1) * blk) {
+        j = 1 + l / blk;
+        loc = l - (j - 1) * blk;
+        if (loc < p.n_g) {
+            r.type = kUnitGrad;
+        } else {
+            r.type = kUnitDW;
+            loc -= p.n_g;
+            j -= 1;
+        }
+    } else {
+        l -= (r.nb - 1) * blk;
+        j = r.nb - 1;
+        if (l < p.n_dh) {
+            r.type = kUnitDH;
+            loc = l;
+        } else {
+            r.type = kUnitDW;
+            loc = l - p.n_dh;
+        }
+    }
+    r.c = r.c0 + j;
+    r.r0 = r.row_idx * static_cast<int>(p.nc_max);
+    r.nc = min(static_cast<int>(p.nc_max), p.n - r.r0);
+    r.gcol = j * static_cast<int>(p.ldg);
+    if (r.type == kUnitDH) {
+        r.vb = r.gl * p.kg * static_cast<int>(p.ldg);
+        r.vc = min(r.nb * static_cast<int>(p.ldg), p.v - r.vb);
+        r.m_blk = loc / p.d_tiles;
+        r.n_tile = loc - r.m_blk * p.d_tiles;
         r.empty = r.m_blk * kPM >= r.nc;
     } else {
-        const int l2 = l - p.n_g - p.n_dh;
-        r.type = kUnitDW;
-        r.n_tile = l2 / p.vm;
-        r.m_blk = l2 - r.n_tile * p.vm;
-        r.empty = r.m_blk * kPM >= r.vc;
+        r.vb = (r.gl * p.kg + j) * static_cast<int>(p.ldg);
+        r.vc = min(static_cast<int>(p.ldg), p.v - r.vb);
+        if (r.type == kUnitGrad) {
+            r.m_blk = loc / p.vt;
+            r.n_tile = loc - r.m_blk * p.vt;
+            r.empty = r.m_blk * kPM >= r.nc || r.n_tile * kBN >= r.vc;
+        } else {
+            r.n_tile = loc / p.vm;
+            r.m_blk = loc - r.n_tile * p.vm;
+            r.empty = r.m_blk * kPM >= r.vc;
+        }
     }
     if (!((p.unit_mask >> r.type) & 1)) r.empty = true;
     return r;
@@ -127,9 +169,10 @@ __device__ __forceinline__ void named_bar_sync(int id, int count) {
     asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(count) : "memory");
 }
 
-// counters: [0] scheduler; chunk c: [1+4c] G done, [2+4c] dH done, [3+4c] dW done,
-// [4+4c] M (dH + dW) done; then per (chunk, 256-row block) G done.  Both CTAs
-// of a pair signal every unit, so every target is twice the unit count.
+// counters: [0] scheduler; chunk c: [1+4c] G done, [2+4c] dH of the group ending
+// at c done, [3+4c] dW done, [4+4c] dH + dW of the group starting at c done;
+// then per (chunk, 256-row block) G done.  Both CTAs of a pair signal every
+// unit, so every target is twice the unit count.
 __device__ __forceinline__ unsigned* cnt(const BwdParams& p, int c, int k) {
     return p.counters + 1 + 4 * c + k;
 }
@@ -223,10 +266,17 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(128 + 32 * kEpiWarps
                 const BUnit un = decode_unit(p, u);
                 if (un.type != kUnitStop && !un.empty) {
                     if (un.type == kUnitGrad) {
-                        if (un.c >= 2) wait_at_least(cnt(p, un.c - 2, 3), two * (p.n_dh + p.n_dw));
+                        const int g = un.row_idx * p.gpr + un.gl;
+                        if (g >= 2) {
+                            // the slot's previous group: g - 2 (possibly in the previous row chunk)
+                            const int g2 = g - 2, r2 = g2 / p.gpr, gl2 = g2 - r2 * p.gpr;
+                            const int nb2 = min(p.kg, p.bands - gl2 * p.kg);
+                            wait_at_least(cnt(p, r2 * p.bands + gl2 * p.kg, 3), two * (p.n_dh + nb2 * p.n_dw));
+                        }
                     } else if (un.type == kUnitDH) {
-                        wait_at_least(p.counters + p.gm_base + un.c * p.mb_max + un.m_blk, two * p.vt);
-                        if (un.band_idx > 0) wait_at_least(cnt(p, un.c - 1, 1), two * p.n_dh);
+                        for (int cc = un.c0; cc <= un.c; ++cc)
+                            wait_at_least(p.counters + p.gm_base + cc * p.mb_max + un.m_blk, two * p.vt);
+                        if (un.gl > 0) wait_at_least(cnt(p, un.c0 - 1, 1), two * p.n_dh);
                     } else {
                         wait_at_least(cnt(p, un.c, 0), two * p.n_g);
                         if (un.row_idx > 0) wait_at_least(cnt(p, un.c - p.bands, 2), two * p.n_dw);
@@ -292,7 +342,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(128 + 32 * kEpiWarps
                     ma = &maps.g_mn;
                     mb = &maps.h_mn;
                     a_mn = b_mn = 1;
-                    a_row = un.m_blk * kPM + rank * 128;
+                    a_row = un.gcol + un.m_blk * kPM + rank * 128;
                     b_row = un.n_tile * kBN + rank * 128;
                     a_k0 = un.slot * static_cast<int>(p.nc_max);
                     b_k0 = un.r0;
@@ -484,7 +534,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(128 + 32 * kEpiWarps
                             fence_proxy_async_shared();
                             named_bar_sync(2 + grp, 128);
                             if (gl) {
-                                tma_store_2d(&maps.g_st, sbuf, un.n_tile * kBN + c64,
+                                tma_store_2d(&maps.g_st, sbuf, un.gcol + un.n_tile * kBN + c64,
                                              un.slot * static_cast<int>(p.nc_max) + un.m_blk * kPM +
                                                  static_cast<int>(rank) * 128);
                                 bulk_commit();
@@ -492,10 +542,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(128 + 32 * kEpiWarps
                         }
                     } else {
                         const bool is_dh = un.type == kUnitDH;
-                        const bool accumulate = is_dh ? (un.band_idx > 0 || p.accumulate_dh) : (un.row_idx > 0);
+                        const bool accumulate = is_dh ? (un.gl > 0 || p.accumulate_dh) : (un.row_idx > 0);
                         const CUtensorMap* om = is_dh ? &maps.dh_st : &maps.dw_st;
                         const int orow = (is_dh ? un.r0 : un.vb) + un.m_blk * kPM + static_cast<int>(rank) * 128;
-                        const bool discard = (p.unit_mask >> 5) & 1;
+                        // debug: bit 5 discards dH and dW writes, bit 6 only dH, bit 7 only dW
+                        const bool discard = ((p.unit_mask >> 5) & 1) || ((p.unit_mask >> (is_dh ? 6 : 7)) & 1);
 #pragma unroll 1
                         for (int sl = 0; sl < ncols / 32; ++sl) {
                             const int c32 = gcol0 + sl * 32;
@@ -534,7 +585,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(128 + 32 * kEpiWarps
                         tcol = y - (p.v_offset + un.vb);
                     }
                     __nv_bfloat16* grow_ptr =
-                        p.g_ring + (static_cast<int64_t>(un.slot) * p.nc_max + lrow) * p.ldg;
+                        p.g_ring + (static_cast<int64_t>(un.slot) * p.nc_max + lrow) * p.ldr + un.gcol;
 #pragma unroll 1
                     for (int cc = 0; cc < kBN / 32 / (kEpiWarps / 4); ++cc) {
                         const int c = chalf * (kBN / 32 / (kEpiWarps / 4)) + cc;
@@ -561,7 +612,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(128 + 32 * kEpiWarps
                     // dH rows = chunk rows into dH; dW rows = band vocab rows into dW
                     const bool is_dh = un.type == kUnitDH;
                     const int mrows = is_dh ? un.nc : un.vc;
-                    const bool accumulate = is_dh ? (un.band_idx > 0 || p.accumulate_dh) : (un.row_idx > 0);
+                    const bool accumulate = is_dh ? (un.gl > 0 || p.accumulate_dh) : (un.row_idx > 0);
                     float* crow = is_dh ? p.dh + (static_cast<int64_t>(un.r0) + lrow) * p.lddh
                                         : p.dw + (static_cast<int64_t>(un.vb) + lrow) * p.lddw;
 #pragma unroll 1
@@ -624,10 +675,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(128 + 32 * kEpiWarps
                     atomicAdd(cnt(p, un.c, 0), 1u);
                 } else if (un.type == kUnitDH) {
                     atomicAdd(cnt(p, un.c, 1), 1u);
-                    atomicAdd(cnt(p, un.c, 3), 1u);
+                    atomicAdd(cnt(p, un.c0, 3), 1u);
                 } else {
                     atomicAdd(cnt(p, un.c, 2), 1u);
-                    atomicAdd(cnt(p, un.c, 3), 1u);
+                    atomicAdd(cnt(p, un.c0, 3), 1u);
                 }
             }
         }

@@ -69,9 +69,10 @@ struct TensorMaps {
 // ----------------------------------------------------------- persistent backward
 // Every (row chunk x vocab band) chunk is laid out at full geometry; see fce_bwd.cu.
 struct BwdParams {
-    int units;               // n_chunks * per_chunk
+    int units;               // row chunks * per_rc
     int n_chunks, bands;     // chunks = row chunks x bands, chunk c = (c / bands, c % bands)
-    int per_chunk;           // n_g + n_dh + n_dw
+    int kg, gpr;             // bands per dH group, dH groups per row chunk
+    int per_rc, per_gf;      // units per row chunk, per full group
     int n_g, n_dh, n_dw;     // grad / dH / dW units per chunk (padded geometry)
     int vt, vm;              // band / 256, band / 128
     int d_tiles, k_blocks_d, mb_max, gm_base;
@@ -82,14 +83,14 @@ struct BwdParams {
     int tma_epi;             // 1: epilogue writes G / dH / dW through SMEM + TMA store / reduce-add
     int l2_hints;            // bit0: evict_first on dH/dW writes, bit1: evict_last on G loads,
                              // bit2: evict_last on G stores, bit3: evict_first on H loads (dW)
-    int64_t nc_max, ldg, d, lddh, lddw, v_offset, ignore_index;
+    int64_t nc_max, ldg, ldr, d, lddh, lddw, v_offset, ignore_index;  // ldg = band, ldr = kg * band
     unsigned* counters;      // [0] scheduler, 4 per chunk, then mb_max per chunk
     unsigned long long* trace;  // dev only: [units][8] = MMA start, MMA end, epilogue end, smid,
                                 //   accumulator free, first stage ready, stage-wait cycles
     const int64_t* targets;
     const float* lse;
     const float* gamma;
-    __nv_bfloat16* g_ring;   // [2][nc_max][ldg]
+    __nv_bfloat16* g_ring;   // [2 group slots][nc_max][ldr]: band j of a group at column j * ldg
     float* dh;
     float* dw;
 };
@@ -98,6 +99,8 @@ struct BwdMaps {
     CUtensorMap h_k, w_k, g_k, w_mn, g_mn, h_mn;
     CUtensorMap g_st, dh_st, dw_st;  // epilogue TMA stores / reduce-adds (tma_epi)
 };
+
+cudaError_t launch_fwd_pair(const TileParams& p, const TensorMaps& maps, int sms, cudaStream_t stream);
 
 cudaError_t launch_pair_gemm(const GemmProblem& q, const TensorMaps& maps, int sms,
                              cudaStream_t stream);

@@ -211,6 +211,38 @@ def test_small_config_with_backward_chunking(cuda):
     h.close()
 
 
+@pytest.mark.parametrize("shape", [(1, 8, 3), (255, 72, 511), (257, 136, 3000), (700, 4096, 1000)])
+def test_forward_cta_pair_variant(cuda, shape):
+    """The cta_group::2 forward (option fwd_pair) against the oracle."""
+    n, d, v = shape
+    H, W, Y, ign, st, rows, lred = _oracle_case(n, d, v, 23, 0.25, "mean")
+    Hd, Wd, Yd = to_dev(H, W, Y)
+    h = fce.Handle(0)
+    h.set_option("fwd_pair", 1)
+    out = fce.fused_forward(Hd, Wd, Yd, "mean", ign, handle=h)
+    check_forward(out, st, rows, lred, Y, ign, "mean")
+    h.close()
+
+
+@pytest.mark.parametrize("kg", [1, 2, 3, 4, 8])
+def test_backward_dh_groups(cuda, kg):
+    """dH contracted over groups of kg bands (ragged last group, short last row
+    chunk, 3 row chunks): same gradients, and bitwise run-to-run identical."""
+    H, W, Y, ign, st, rows, lred = _oracle_case(700, 136, 3000, 9, 0.25, "mean")
+    Hd, Wd, Yd = to_dev(H, W, Y)
+    h = fce.Handle(0)
+    h.set_option("row_chunk", 256)
+    h.set_option("band_cols", 512)
+    h.set_option("dh_group", kg)
+    out = fce.fused_forward(Hd, Wd, Yd, "mean", ign, handle=h)
+    dH, dW = ob.backward(H, W, Y, st, "mean", 1.0, ign)
+    dh, dw = fce.fused_backward_recompute(Hd, Wd, Yd, out.stats, "mean", 1.0, ign, handle=h)
+    check_grads(dh, dw, dH, dW, Y, ign)
+    dh2, dw2 = fce.fused_backward_recompute(Hd, Wd, Yd, out.stats, "mean", 1.0, ign, handle=h)
+    assert torch.equal(dh, dh2) and torch.equal(dw, dw2)
+    h.close()
+
+
 @pytest.mark.parametrize("window", [1, 3, 16, 128, 256, 257, 1000])
 def test_windowed_forward(cuda, window):
     # window sweep {1,3,16,128,256,257} (test_fused_forward.cpp:146-175)
