@@ -55,6 +55,7 @@ struct fce_handle_s {
     int64_t splits = 0, band_cols = 0, row_chunk = 0, validate = 1, bwd_persistent = 1;
     int64_t l2_hints = 1;
     int64_t gemm_pair = 1;
+    int64_t fwd_m_group = 0;  // forward raster: row blocks per L2 group (0 = default)
     int64_t fwd_pair = 0;     // forward on CTA pairs (fce_fwd_pair.cu); measured slower under the power cap
     int64_t bwd_unit_mask = 7;
     int64_t trace_ptr = 0;
@@ -277,7 +278,7 @@ fce_status run_forward_tiles(fce_handle h, const fce_problem* p, const FwdGeom& 
     tp.m_blocks = static_cast<int>(g.m_blocks);
     tp.v_tiles = static_cast<int>(g.v_tiles);
     tp.splits = g.splits;
-    tp.m_group = std::min(tp.m_blocks, g.pair ? 8 : 16);
+    tp.m_group = static_cast<int>(std::min<int64_t>(tp.m_blocks, h->fwd_m_group ? h->fwd_m_group : (g.pair ? 8 : 32)));
     tp.k_blocks = static_cast<int>(ceil_div(p->d, kBK));
     tp.units = tp.m_blocks * tp.splits;
     tp.targets = p->targets;
@@ -506,6 +507,8 @@ fce_status fce_set_option(fce_handle h, const char* key, int64_t value) {
     } else if (!std::strcmp(key, "dh_group")) {
         if (value < 1 || value > 64) return fail(FCE_INVALID_ARGUMENT, "dh_group must be in [1, 64]");
         h->dh_group = value;
+    } else if (!std::strcmp(key, "fwd_m_group")) {
+        h->fwd_m_group = value;
     } else if (!std::strcmp(key, "fwd_pair")) {
         h->fwd_pair = value ? 1 : 0;
     } else if (!std::strcmp(key, "gemm_pair")) {
