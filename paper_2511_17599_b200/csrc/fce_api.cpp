@@ -61,7 +61,11 @@ struct fce_handle_s {
     int64_t trace_ptr = 0;
     int64_t bwd_epi_warps = 8;
     int64_t bwd_tma_epi = 1;
-    int64_t dh_group = 1;     // bands per dH group in the persistent backward  // dev only: device buffer for per-unit timestamps
+    int64_t dh_group = 1;     // bands per dH group in the persistent backward
+    int64_t skip_ignored = 1; // compact away ignored rows before the tile kernels
+    // compaction buffers (grow-only, separate from ws so both can be live)
+    void* cws = nullptr;
+    size_t cws_size = 0;
     int64_t launches = 0;
     size_t bwd_scratch[4] = {0, 0, 0, 0};  // offsets of the persistent-backward scratch
     // optional per-kernel CUDA-event timing of the tile kernels (bench roofline)
@@ -87,8 +91,11 @@ namespace {
 
 struct Scratch {
     fce_handle h;
+    void** buf;
+    size_t* size;
     size_t off = 0;
-    explicit Scratch(fce_handle hh) : h(hh) {}
+    explicit Scratch(fce_handle hh) : h(hh), buf(&hh->ws), size(&hh->ws_size) {}
+    Scratch(fce_handle hh, void** b, size_t* sz) : h(hh), buf(b), size(sz) {}
     // Carves 256-byte aligned pieces out of the handle workspace; call
     // commit() once the layout is known so the workspace grows in one go.
     size_t take(size_t bytes) {
@@ -97,26 +104,26 @@ struct Scratch {
         return o;
     }
     fce_status commit() {
-        if (off > h->ws_size) {
-            if (h->ws) {
+        if (off > *size) {
+            if (*buf) {
                 cudaStreamSynchronize(h->stream);
-                cudaFree(h->ws);
-                h->ws = nullptr;
-                h->ws_size = 0;
+                cudaFree(*buf);
+                *buf = nullptr;
+                *size = 0;
             }
-            cudaError_t e = cudaMalloc(&h->ws, off);
+            cudaError_t e = cudaMalloc(buf, off);
             if (e != cudaSuccess)
                 return fail(FCE_CUDA_ERROR, "workspace allocation of %zu bytes failed: %s", off,
                             cudaGetErrorString(e));
-            h->ws_size = off;
+            *size = off;
         }
-        h->ws_in_use = off;
-        h->ws_peak = std::max(h->ws_peak, off + 64 + 3 * sizeof(int) * kErrSlots);
+        if (buf == &h->ws) h->ws_in_use = off;
+        h->ws_peak = std::max(h->ws_peak, h->ws_size + h->cws_size + 64 + 3 * sizeof(int) * kErrSlots);
         return FCE_OK;
     }
     template <typename T>
     T* ptr(size_t o) const {
-        return reinterpret_cast<T*>(static_cast<char*>(h->ws) + o);
+        return reinterpret_cast<T*>(static_cast<char*>(*buf) + o);
     }
 };
 
@@ -173,6 +180,76 @@ fce_status read_errors(fce_handle h, bool sync) {
 
 fce_status reset_flags(fce_handle h) {
     FCE_CUDA(cudaMemsetAsync(h->err, 0, sizeof(int) * kErrSlots + 64, h->stream));
+    return FCE_OK;
+}
+
+// Ignored-row compaction (the reference skips ignored positions outright,
+// fused_forward.hpp:57-59, fused_backward.hpp:37-39): when the targets carry
+// ignored rows, the tile kernels run on the valid rows only.  The valid count
+// is read back to size the compact problem (one stream sync, the same the
+// validation already does by default).
+struct Compact {
+    bool on = false;
+    int64_t n_valid = 0;
+    int* map = nullptr;        // [N] slot or -1
+    int* rows = nullptr;       // [n_valid] original row
+    int64_t* targets = nullptr;
+    void* hidden = nullptr;    // [n_valid, ldh] bf16
+    int64_t ldh = 0;
+    float* gamma = nullptr;    // backward: per-slot effective upstream / lse
+    float* lse = nullptr;
+    float* dh = nullptr;       // backward: [n_valid, lddh] fp32
+    int64_t lddh = 0;
+};
+
+fce_status plan_compaction(fce_handle h, const fce_problem* p, bool backward, bool want_dh, Compact* c,
+                           fce_problem* pc) {
+    *pc = *p;
+    if (!p->has_ignore || !h->skip_ignored) return FCE_OK;
+    FCE_CUDA(cudaMemcpyAsync(h->host_err + kErrSlots, h->count, sizeof(unsigned long long),
+                             cudaMemcpyDeviceToHost, h->stream));
+    FCE_CUDA(cudaStreamSynchronize(h->stream));
+    unsigned long long cnt;
+    std::memcpy(&cnt, h->host_err + kErrSlots, sizeof(cnt));
+    const int64_t nv = static_cast<int64_t>(cnt);
+    if (nv >= p->n) return FCE_OK;
+    c->on = true;
+    c->n_valid = nv;
+    c->ldh = round_up(p->d, 8);
+    c->lddh = round_up(p->d, 4);
+    Scratch cs(h, &h->cws, &h->cws_size);
+    const size_t o_map = cs.take(sizeof(int) * p->n);
+    const size_t o_rows = cs.take(sizeof(int) * std::max<int64_t>(nv, 1));
+    const size_t o_t = cs.take(sizeof(int64_t) * std::max<int64_t>(nv, 1));
+    const size_t o_h = cs.take(sizeof(__nv_bfloat16) * std::max<int64_t>(nv, 1) * c->ldh);
+    size_t o_g = 0, o_l = 0, o_dh = 0;
+    if (backward) {
+        o_g = cs.take(sizeof(float) * std::max<int64_t>(nv, 1));
+        o_l = cs.take(sizeof(float) * std::max<int64_t>(nv, 1));
+        if (want_dh) o_dh = cs.take(sizeof(float) * std::max<int64_t>(nv, 1) * c->lddh);
+    }
+    fce_status s = cs.commit();
+    if (s) return s;
+    c->map = cs.ptr<int>(o_map);
+    c->rows = cs.ptr<int>(o_rows);
+    c->targets = cs.ptr<int64_t>(o_t);
+    c->hidden = cs.ptr<void>(o_h);
+    if (backward) {
+        c->gamma = cs.ptr<float>(o_g);
+        c->lse = cs.ptr<float>(o_l);
+        if (want_dh) c->dh = cs.ptr<float>(o_dh);
+    }
+    cudaError_t e = launch_row_map(p->targets, p->n, p->ignore_index, c->map, c->rows, h->stream);
+    if (e == cudaSuccess)
+        e = launch_gather_rows(p->hidden, p->ldh * 2, c->hidden, c->ldh * 2, p->d * 2, c->rows, nv,
+                               p->targets, c->targets, nullptr, nullptr, nullptr, nullptr, h->stream);
+    if (e != cudaSuccess) return fail(FCE_CUDA_ERROR, "compaction kernels: %s", cudaGetErrorString(e));
+    h->launches += nv > 0 ? 3 : 1;
+    pc->hidden = c->hidden;
+    pc->ldh = c->ldh;
+    pc->n = nv;
+    pc->targets = c->targets;
+    pc->has_ignore = 0;
     return FCE_OK;
 }
 
@@ -453,7 +530,7 @@ fce_status fce_create(fce_handle* out, int device, void* stream) {
     }
     h->count = reinterpret_cast<unsigned long long*>(reinterpret_cast<char*>(h->err) +
                                                      sizeof(int) * kErrSlots);
-    e = cudaMallocHost(&h->host_err, sizeof(int) * kErrSlots);
+    e = cudaMallocHost(&h->host_err, sizeof(int) * kErrSlots + 64);
     if (e != cudaSuccess) {
         cudaFree(h->err);
         delete h;
@@ -470,6 +547,7 @@ fce_status fce_destroy(fce_handle h) {
     drain_timing(h);
     for (cudaEvent_t e : h->event_pool) cudaEventDestroy(e);
     if (h->ws) cudaFree(h->ws);
+    if (h->cws) cudaFree(h->cws);
     if (h->err) cudaFree(h->err);
     if (h->host_err) cudaFreeHost(h->host_err);
     delete h;
@@ -507,6 +585,8 @@ fce_status fce_set_option(fce_handle h, const char* key, int64_t value) {
     } else if (!std::strcmp(key, "dh_group")) {
         if (value < 1 || value > 64) return fail(FCE_INVALID_ARGUMENT, "dh_group must be in [1, 64]");
         h->dh_group = value;
+    } else if (!std::strcmp(key, "skip_ignored")) {
+        h->skip_ignored = value ? 1 : 0;
     } else if (!std::strcmp(key, "fwd_m_group")) {
         h->fwd_m_group = value;
     } else if (!std::strcmp(key, "fwd_pair")) {
@@ -565,26 +645,32 @@ fce_status fce_forward(fce_handle h, const fce_problem* p, int reduction, int64_
     if (e != cudaSuccess) return fail(FCE_CUDA_ERROR, "prep kernel: %s", cudaGetErrorString(e));
     h->launches += 1;
     if ((s = read_errors(h, h->validate != 0))) return s;
+    Compact cp;
+    fce_problem pc;
+    if ((s = plan_compaction(h, p, false, false, &cp, &pc))) return s;
+    const int64_t nc = std::max<int64_t>(pc.n, 1);  // partial rows (>= 1 keeps pointers valid)
 
-    const FwdGeom geom = forward_geometry(h, p, window);
-    const int splits = geom.splits;
+    const FwdGeom geom = forward_geometry(h, &pc, window);
+    const int splits = std::max(geom.splits, 1);
 
     Scratch sc(h);
-    const size_t o_m = sc.take(sizeof(float) * splits * p->n);
-    const size_t o_a = sc.take(sizeof(float) * splits * p->n);
-    const size_t o_z = sc.take(sizeof(float) * splits * p->n);
-    const size_t o_f = sc.take(splits * p->n);
+    const size_t o_m = sc.take(sizeof(float) * splits * nc);
+    const size_t o_a = sc.take(sizeof(float) * splits * nc);
+    const size_t o_z = sc.take(sizeof(float) * splits * nc);
+    const size_t o_f = sc.take(splits * nc);
     const size_t o_b = sc.take(sizeof(double) * (ceil_div(p->n, 256) + 1));
     if ((s = sc.commit())) return s;
 
-    if ((s = run_forward_tiles(h, p, geom, sc.ptr<float>(o_m), sc.ptr<float>(o_a),
+    if (pc.n > 0 &&
+        (s = run_forward_tiles(h, &pc, geom, sc.ptr<float>(o_m), sc.ptr<float>(o_a),
                                sc.ptr<float>(o_z), sc.ptr<uint8_t>(o_f))))
         return s;
     int blocks = 0;
-    e = launch_merge_stats(splits, p->n, p->n, sc.ptr<float>(o_m), sc.ptr<float>(o_a),
+    e = launch_merge_stats(splits, p->n, nc, sc.ptr<float>(o_m), sc.ptr<float>(o_a),
                            sc.ptr<float>(o_z), sc.ptr<uint8_t>(o_f), p->targets, p->has_ignore,
                            p->ignore_index, 1, stats.m, stats.a, stats.z_target, stats.found, lse,
-                           loss_rows, sc.ptr<double>(o_b), h->err, h->stream, &blocks);
+                           loss_rows, sc.ptr<double>(o_b), h->err, h->stream, &blocks,
+                           cp.on ? cp.map : nullptr);
     if (e != cudaSuccess) return fail(FCE_CUDA_ERROR, "merge kernel: %s", cudaGetErrorString(e));
     h->launches += 1;
     if (reduction != FCE_REDUCTION_NONE && loss_reduced) {
@@ -606,21 +692,27 @@ fce_status fce_forward_partial(fce_handle h, const fce_problem* p, fce_stats par
     if (e != cudaSuccess) return fail(FCE_CUDA_ERROR, "prep kernel: %s", cudaGetErrorString(e));
     h->launches += 1;
     if ((s = read_errors(h, h->validate != 0))) return s;
-    const FwdGeom geom = forward_geometry(h, p, 0);
-    const int splits = geom.splits;
+    Compact cp;
+    fce_problem pc;
+    if ((s = plan_compaction(h, p, false, false, &cp, &pc))) return s;
+    const int64_t nc = std::max<int64_t>(pc.n, 1);
+    const FwdGeom geom = forward_geometry(h, &pc, 0);
+    const int splits = std::max(geom.splits, 1);
     Scratch sc(h);
-    const size_t o_m = sc.take(sizeof(float) * splits * p->n);
-    const size_t o_a = sc.take(sizeof(float) * splits * p->n);
-    const size_t o_z = sc.take(sizeof(float) * splits * p->n);
-    const size_t o_f = sc.take(splits * p->n);
+    const size_t o_m = sc.take(sizeof(float) * splits * nc);
+    const size_t o_a = sc.take(sizeof(float) * splits * nc);
+    const size_t o_z = sc.take(sizeof(float) * splits * nc);
+    const size_t o_f = sc.take(splits * nc);
     if ((s = sc.commit())) return s;
-    if ((s = run_forward_tiles(h, p, geom, sc.ptr<float>(o_m), sc.ptr<float>(o_a),
+    if (pc.n > 0 &&
+        (s = run_forward_tiles(h, &pc, geom, sc.ptr<float>(o_m), sc.ptr<float>(o_a),
                                sc.ptr<float>(o_z), sc.ptr<uint8_t>(o_f))))
         return s;
-    e = launch_merge_stats(splits, p->n, p->n, sc.ptr<float>(o_m), sc.ptr<float>(o_a),
+    e = launch_merge_stats(splits, p->n, nc, sc.ptr<float>(o_m), sc.ptr<float>(o_a),
                            sc.ptr<float>(o_z), sc.ptr<uint8_t>(o_f), p->targets, p->has_ignore,
                            p->ignore_index, 0, partial.m, partial.a, partial.z_target, partial.found,
-                           nullptr, nullptr, nullptr, h->err, h->stream, nullptr);
+                           nullptr, nullptr, nullptr, h->err, h->stream, nullptr,
+                           cp.on ? cp.map : nullptr);
     if (e != cudaSuccess) return fail(FCE_CUDA_ERROR, "merge kernel: %s", cudaGetErrorString(e));
     h->launches += 1;
     return FCE_OK;
@@ -661,6 +753,11 @@ fce_status fce_merge_partials(fce_handle h, int parts, int64_t n, int64_t part_s
     return read_errors(h, h->validate != 0);
 }
 
+static fce_status run_backward_tiles(fce_handle h, const fce_problem* p, const float* gamma,
+                                     const float* lse, int64_t row_chunk, int64_t band, __nv_bfloat16* G,
+                                     float* dhidden, int64_t lddh, float* dweight, int64_t lddw,
+                                     int accumulate_dhidden);
+
 fce_status fce_backward(fce_handle h, const fce_problem* p, fce_stats stats, int reduction,
                         float upstream_scalar, const float* upstream_rows, float* dhidden,
                         int64_t lddh, float* dweight, int64_t lddw, int accumulate_dhidden) {
@@ -678,10 +775,22 @@ fce_status fce_backward(fce_handle h, const fce_problem* p, fce_stats stats, int
     if (dweight && lddw < p->d) return fail(FCE_DIMENSION_MISMATCH, "lddw < d");
     const int64_t v_total = p->v_total ? p->v_total : p->v;
 
+    if ((s = reset_flags(h))) return s;
+    cudaError_t e = launch_prep_targets(p->targets, p->n, p->has_ignore, p->ignore_index, v_total,
+                                        h->err, h->count, h->stream);
+    if (e != cudaSuccess) return fail(FCE_CUDA_ERROR, "prep kernel: %s", cudaGetErrorString(e));
+    h->launches += 1;
+    // ignored rows compacted away (their gradient rows are exactly zero)
+    Compact cp;
+    fce_problem pcv;
+    if ((s = plan_compaction(h, p, true, dhidden != nullptr, &cp, &pcv))) return s;
+    const fce_problem* pk = &pcv;  // the problem the tile kernels see
+    const int64_t n_k = std::max<int64_t>(pk->n, 1);
+
     // chunking of G = N_c x V_c bf16
     // defaults measured best on B200 at the Llama-3-8B shape
     int64_t row_chunk = h->row_chunk ? h->row_chunk : 16384;
-    row_chunk = std::min(row_chunk, round_up(p->n, h->bwd_persistent ? 256 : kBM));
+    row_chunk = std::min(row_chunk, round_up(n_k, h->bwd_persistent ? 256 : kBM));
     if (h->bwd_persistent) row_chunk = round_up(row_chunk, 256);
     int64_t band = h->band_cols;
     if (!band) {
@@ -698,7 +807,7 @@ fce_status fce_backward(fce_handle h, const fce_problem* p, fce_stats stats, int
     const size_t o_g = sc.take(sizeof(float) * p->n);
     const size_t o_l = sc.take(sizeof(float) * p->n);
     const size_t o_G = sc.take(sizeof(__nv_bfloat16) * row_chunk * band * (h->bwd_persistent ? 2 * kg : 1));
-    const int64_t n_rc = ceil_div(p->n, row_chunk), n_bd = ceil_div(p->v, band);
+    const int64_t n_rc = ceil_div(n_k, row_chunk), n_bd = ceil_div(p->v, band);
     const int64_t n_chunks = n_rc * n_bd;
     const int64_t mb_max = ceil_div(row_chunk, 128);
     const size_t o_tab = 0, o_bnd = 0;
@@ -712,21 +821,57 @@ fce_status fce_backward(fce_handle h, const fce_problem* p, fce_stats stats, int
     float* lse = sc.ptr<float>(o_l);
     __nv_bfloat16* G = sc.ptr<__nv_bfloat16>(o_G);
 
-    if ((s = reset_flags(h))) return s;
-    cudaError_t e = launch_prep_targets(p->targets, p->n, p->has_ignore, p->ignore_index, v_total,
-                                        h->err, h->count, h->stream);
-    if (e != cudaSuccess) return fail(FCE_CUDA_ERROR, "prep kernel: %s", cudaGetErrorString(e));
     e = launch_gamma(p->n, p->targets, p->has_ignore, p->ignore_index, stats.m, stats.a, stats.found,
                      reduction, upstream_scalar, upstream_rows, h->count, gamma, lse, h->err, h->stream);
     if (e != cudaSuccess) return fail(FCE_CUDA_ERROR, "gamma kernel: %s", cudaGetErrorString(e));
-    h->launches += 2;
+    h->launches += 1;
     if ((s = read_errors(h, h->validate != 0))) return s;
     if (!dhidden && !dweight) return FCE_OK;
 
-    if (h->bwd_persistent)
-        return run_backward_persistent(h, p, gamma, lse, row_chunk, band, kg, dhidden, lddh, dweight,
-                                       lddw, accumulate_dhidden);
+    float* dh_k = dhidden;
+    int64_t lddh_k = lddh;
+    int acc_k = accumulate_dhidden;
+    if (cp.on) {
+        e = launch_gather_rows(nullptr, 0, nullptr, 0, 0, cp.rows, cp.n_valid, nullptr, nullptr, gamma,
+                               cp.gamma, lse, cp.lse, h->stream);
+        if (e != cudaSuccess) return fail(FCE_CUDA_ERROR, "compaction gather: %s", cudaGetErrorString(e));
+        h->launches += cp.n_valid > 0 ? 1 : 0;
+        gamma = cp.gamma;
+        lse = cp.lse;
+        dh_k = cp.dh;
+        lddh_k = cp.lddh;
+        acc_k = 0;
+        if (cp.n_valid == 0 && dweight) {
+            // nothing valid: dW is exactly zero (zero-initialised, never accumulated)
+            FCE_CUDA(cudaMemset2DAsync(dweight, lddw * sizeof(float), 0, p->d * sizeof(float), p->v, h->stream));
+        }
+    }
+    if (pk->n > 0) {
+        if (h->bwd_persistent) {
+            s = run_backward_persistent(h, pk, gamma, lse, row_chunk, band, kg, dh_k, lddh_k, dweight,
+                                        lddw, acc_k);
+        } else {
+            s = run_backward_tiles(h, pk, gamma, lse, row_chunk, band, G, dh_k, lddh_k, dweight, lddw,
+                                   acc_k);
+        }
+        if (s) return s;
+    }
+    if (cp.on && dhidden) {
+        e = launch_scatter_rows_f32(cp.dh, cp.lddh, dhidden, lddh, p->d, cp.map, p->n, accumulate_dhidden,
+                                    h->stream);
+        if (e != cudaSuccess) return fail(FCE_CUDA_ERROR, "scatter kernel: %s", cudaGetErrorString(e));
+        h->launches += 1;
+    }
+    return FCE_OK;
+}
 
+// Non-persistent backward (option bwd_persistent = 0): per (row chunk, band)
+// a G tile launch and one dW / dH GEMM launch.
+static fce_status run_backward_tiles(fce_handle h, const fce_problem* p, const float* gamma,
+                                     const float* lse, int64_t row_chunk, int64_t band, __nv_bfloat16* G,
+                                     float* dhidden, int64_t lddh, float* dweight, int64_t lddw,
+                                     int accumulate_dhidden) {
+    cudaError_t e;
     const int k_blocks_d = static_cast<int>(ceil_div(p->d, kBK));
     for (int64_t r0 = 0; r0 < p->n; r0 += row_chunk) {
         const int64_t nc = std::min(row_chunk, p->n - r0);

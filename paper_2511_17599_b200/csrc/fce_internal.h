@@ -129,7 +129,17 @@ cudaError_t launch_merge_stats(int parts, int64_t n, int64_t part_stride, const 
                                const int64_t* targets, int has_ignore, int64_t ignore_index,
                                int emit_loss, float* m, float* a, float* zt, uint8_t* found,
                                float* lse, float* loss_rows, double* block_sums, int* err_flags,
-                               cudaStream_t stream, int* blocks_out);
+                               cudaStream_t stream, int* blocks_out, const int* row_map = nullptr);
+// ignored-row compaction (fce_kernels.cu)
+cudaError_t launch_row_map(const int64_t* targets, int64_t n, int64_t ignore_index, int* row_map,
+                           int* rows, cudaStream_t stream);
+cudaError_t launch_gather_rows(const void* src, int64_t ld_src_bytes, void* dst, int64_t ld_dst_bytes,
+                               int64_t row_bytes, const int* rows, int64_t n_rows,
+                               const int64_t* t_in, int64_t* t_out, const float* g_in, float* g_out,
+                               const float* l_in, float* l_out, cudaStream_t stream);
+cudaError_t launch_scatter_rows_f32(const float* src, int64_t ld_src, float* dst, int64_t ld_dst,
+                                    int64_t cols, const int* row_map, int64_t n, int accumulate,
+                                    cudaStream_t stream);
 cudaError_t launch_reduce_loss(const double* block_sums, int blocks,
                                const unsigned long long* valid_count, int reduction,
                                float* loss_reduced, cudaStream_t stream);

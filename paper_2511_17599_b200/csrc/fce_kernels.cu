@@ -466,16 +466,19 @@ __global__ void k_merge_stats(int parts, int64_t n, int64_t stride, const float*
                               const uint8_t* __restrict__ pf, const int64_t* __restrict__ targets,
                               int has_ignore, int64_t ignore_index, int emit_loss, float* m_out,
                               float* a_out, float* zt_out, uint8_t* f_out, float* lse_out,
-                              float* loss_rows, double* block_sums, int* err) {
+                              float* loss_rows, double* block_sums, int* err,
+                              const int* __restrict__ row_map) {
     const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     double my_loss = 0.0;
     if (i < n) {
         const bool ign = has_ignore && targets[i] == ignore_index;
         float M = -INFINITY, A = 0.f, Z = 0.f;
         bool F = false;
+        // partials of compacted problems are indexed by the row's compact slot
+        const int64_t src = row_map ? static_cast<int64_t>(row_map[i]) : i;
         if (!ign) {
             for (int s = 0; s < parts; ++s) {
-                const int64_t o = s * stride + i;
+                const int64_t o = s * stride + src;
                 const float sm = pm[o], sa = pa[o];
                 const bool sf = pf[o] != 0;
                 if (F && sf) atomicOr(&err[kErrDuplicate], 1);
@@ -523,12 +526,145 @@ cudaError_t launch_merge_stats(int parts, int64_t n, int64_t part_stride, const 
                                const int64_t* targets, int has_ignore, int64_t ignore_index,
                                int emit_loss, float* m, float* a, float* zt, uint8_t* found,
                                float* lse, float* loss_rows, double* block_sums, int* err_flags,
-                               cudaStream_t stream, int* blocks_out) {
+                               cudaStream_t stream, int* blocks_out, const int* row_map) {
     const int blocks = static_cast<int>((n + 255) / 256);
     if (blocks_out) *blocks_out = blocks;
     k_merge_stats<<<blocks, 256, 0, stream>>>(parts, n, part_stride, pm, pa, pzt, pf, targets,
                                               has_ignore, ignore_index, emit_loss, m, a, zt, found,
-                                              lse, loss_rows, block_sums, err_flags);
+                                              lse, loss_rows, block_sums, err_flags, row_map);
+    return cudaGetLastError();
+}
+
+// ------------------------------------------------- ignored-row compaction
+// The reference never touches an ignored position: accumulate_stats_block and
+// accumulate_grads_block skip rows whose tracking entry is kSkipPosition
+// (fused_forward.hpp:57-59, fused_backward.hpp:37-39).  The device path gets
+// the same saving by compacting the valid rows before the tile kernels:
+// row_map[i] = slot of row i among the valid rows (ascending), -1 if ignored;
+// rows[j] = original index of slot j.  One block scans N in 1024-row tiles.
+__global__ void __launch_bounds__(1024) k_row_map(const int64_t* __restrict__ targets, int64_t n,
+                                                  int64_t ignore_index, int* row_map, int* rows) {
+    __shared__ int warp_sums[32];
+    __shared__ int base_s;
+    if (threadIdx.x == 0) base_s = 0;
+    __syncthreads();
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    for (int64_t t0 = 0; t0 < n; t0 += 1024) {
+        const int64_t i = t0 + threadIdx.x;
+        const int valid = (i < n && targets[i] != ignore_index) ? 1 : 0;
+        const unsigned bal = __ballot_sync(0xffffffffu, valid);
+        const int in_warp = __popc(bal & ((1u << lane) - 1u));
+        if (lane == 0) warp_sums[wid] = __popc(bal);
+        __syncthreads();
+        if (wid == 0) {
+            const int x = warp_sums[lane];
+            int incl = x;
+            for (int o = 1; o < 32; o <<= 1) {
+                const int y = __shfl_up_sync(0xffffffffu, incl, o);
+                if (lane >= o) incl += y;
+            }
+            warp_sums[lane] = incl - x;  // exclusive
+        }
+        __syncthreads();
+        const int slot = base_s + warp_sums[wid] + in_warp;
+        if (i < n) {
+            row_map[i] = valid ? slot : -1;
+            if (valid) rows[slot] = static_cast<int>(i);
+        }
+        __syncthreads();
+        if (threadIdx.x == 1023) base_s = slot + valid;
+        __syncthreads();
+    }
+}
+
+cudaError_t launch_row_map(const int64_t* targets, int64_t n, int64_t ignore_index, int* row_map,
+                           int* rows, cudaStream_t stream) {
+    k_row_map<<<1, 1024, 0, stream>>>(targets, n, ignore_index, row_map, rows);
+    return cudaGetLastError();
+}
+
+// dst[j, 0:cols) = src[rows[j], 0:cols) for 16-byte elements (cols16 per row)
+__global__ void k_gather_rows16(const uint4* __restrict__ src, int64_t ld_src16, uint4* __restrict__ dst,
+                                int64_t ld_dst16, int64_t cols16, const int* __restrict__ rows,
+                                int64_t n_rows) {
+    const int64_t total = n_rows * cols16;
+    for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < total;
+         k += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t j = k / cols16, c = k - j * cols16;
+        dst[j * ld_dst16 + c] = src[static_cast<int64_t>(rows[j]) * ld_src16 + c];
+    }
+}
+
+// per-slot row data: targets, and (backward) gamma / lse of the valid rows
+__global__ void k_gather_row_scalars(const int* __restrict__ rows, int64_t n_rows,
+                                     const int64_t* __restrict__ t_in, int64_t* t_out,
+                                     const float* __restrict__ g_in, float* g_out,
+                                     const float* __restrict__ l_in, float* l_out) {
+    for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < n_rows;
+         j += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t i = rows[j];
+        if (t_out) t_out[j] = t_in[i];
+        if (g_out) g_out[j] = g_in[i];
+        if (l_out) l_out[j] = l_in[i];
+    }
+}
+
+cudaError_t launch_gather_rows(const void* src, int64_t ld_src_bytes, void* dst, int64_t ld_dst_bytes,
+                               int64_t row_bytes, const int* rows, int64_t n_rows,
+                               const int64_t* t_in, int64_t* t_out, const float* g_in, float* g_out,
+                               const float* l_in, float* l_out, cudaStream_t stream) {
+    if (n_rows <= 0) return cudaSuccess;
+    if (src) {
+        const int64_t cols16 = (row_bytes + 15) / 16;
+        const int64_t total = n_rows * cols16;
+        const int blocks = static_cast<int>(std::min<int64_t>((total + 255) / 256, 148 * 16));
+        k_gather_rows16<<<blocks, 256, 0, stream>>>(static_cast<const uint4*>(src), ld_src_bytes / 16,
+                                                    static_cast<uint4*>(dst), ld_dst_bytes / 16, cols16,
+                                                    rows, n_rows);
+    }
+    const int blocks = static_cast<int>(std::min<int64_t>((n_rows + 255) / 256, 148 * 4));
+    k_gather_row_scalars<<<blocks, 256, 0, stream>>>(rows, n_rows, t_in, t_out, g_in, g_out, l_in, l_out);
+    return cudaGetLastError();
+}
+
+// dH[i, :] = dH_c[row_map[i], :] (or += with accumulate); ignored rows are
+// zeroed (left untouched with accumulate), as accumulate_grads_block leaves
+// them (fused_backward.hpp:37-39 on zero-initialised gradients).
+__global__ void k_scatter_rows_f32(const float* __restrict__ src, int64_t ld_src, float* dst,
+                                   int64_t ld_dst, int64_t cols, const int* __restrict__ row_map,
+                                   int64_t n, int accumulate) {
+    const int64_t c4 = (cols + 3) / 4;
+    const bool vec = (cols % 4 == 0) && (ld_src % 4 == 0) && (ld_dst % 4 == 0);
+    const int64_t total = n * (vec ? c4 : cols);
+    for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < total;
+         k += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t per = vec ? c4 : cols;
+        const int64_t i = k / per, c = k - i * per;
+        const int j = row_map[i];
+        if (j < 0 && accumulate) continue;
+        if (vec) {
+            float4 v = j >= 0 ? reinterpret_cast<const float4*>(src + j * ld_src)[c] : make_float4(0.f, 0.f, 0.f, 0.f);
+            float4* d = reinterpret_cast<float4*>(dst + i * ld_dst) + c;
+            if (accumulate) {
+                const float4 o = *d;
+                v.x += o.x; v.y += o.y; v.z += o.z; v.w += o.w;
+            }
+            *d = v;
+        } else {
+            const float v = j >= 0 ? src[j * ld_src + c] : 0.f;
+            float* d = dst + i * ld_dst + c;
+            *d = accumulate ? *d + v : v;
+        }
+    }
+}
+
+cudaError_t launch_scatter_rows_f32(const float* src, int64_t ld_src, float* dst, int64_t ld_dst,
+                                    int64_t cols, const int* row_map, int64_t n, int accumulate,
+                                    cudaStream_t stream) {
+    const int64_t total = n * ((cols + 3) / 4);
+    const int blocks = static_cast<int>(std::min<int64_t>((total + 255) / 256, 148 * 16));
+    k_scatter_rows_f32<<<std::max(blocks, 1), 256, 0, stream>>>(src, ld_src, dst, ld_dst, cols, row_map, n,
+                                                                accumulate);
     return cudaGetLastError();
 }
 

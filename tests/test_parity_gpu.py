@@ -362,6 +362,40 @@ def test_ignored_row_equals_dropped_row(cuda):
     assert torch.count_nonzero(dh[torch.from_numpy(~keep).cuda()]).item() == 0
 
 
+@pytest.mark.parametrize("n,d,v,frac", [(300, 136, 1500, 0.25), (513, 64, 700, 0.9), (1000, 72, 3000, 0.5),
+                                        (129, 8, 300, 0.01)])
+def test_ignored_row_compaction_matches_full_rows(cuda, n, d, v, frac):
+    """skip_ignored (the default) runs the tile kernels on the valid rows only, as
+    the reference skips ignored positions (fused_forward.hpp:57-59,
+    fused_backward.hpp:37-39); results equal the full-row path and the oracle."""
+    H, W, Y, ign, st, rows, lred = _oracle_case(n, d, v, 31, frac, "mean")
+    Hd, Wd, Yd = to_dev(H, W, Y)
+    hc = fce.Handle(0)
+    hf = fce.Handle(0)
+    hf.set_option("skip_ignored", 0)
+    oc = fce.fused_forward(Hd, Wd, Yd, "mean", ign, handle=hc)
+    of = fce.fused_forward(Hd, Wd, Yd, "mean", ign, handle=hf)
+    check_forward(oc, st, rows, lred, Y, ign, "mean")
+    assert torch.equal(oc.stats.found, of.stats.found)
+    assert abs(oc.loss.item() - of.loss.item()) <= 1e-6 * abs(of.loss.item())
+    dH, dW = ob.backward(H, W, Y, st, "mean", 1.0, ign)
+    dhc, dwc = fce.fused_backward_recompute(Hd, Wd, Yd, oc.stats, "mean", 1.0, ign, handle=hc)
+    dhf, dwf = fce.fused_backward_recompute(Hd, Wd, Yd, of.stats, "mean", 1.0, ign, handle=hf)
+    check_grads(dhc, dwc, dH, dW, Y, ign)
+    assert relmax(dhc.cpu().numpy(), dhf.cpu().numpy()) < 1e-5
+    assert relmax(dwc.cpu().numpy(), dwf.cpu().numpy()) < 1e-5
+    # accumulate_dhidden: ignored rows untouched, valid rows += their gradient
+    base = torch.full_like(dhc, 0.5)
+    acc = base.clone()
+    fce.fused_backward_recompute(Hd, Wd, Yd, oc.stats, "mean", 1.0, ign, handle=hc, dhidden=acc,
+                                 accumulate_dhidden=True)
+    ignored = torch.from_numpy(Y == ign).cuda()
+    assert torch.equal(acc[ignored], base[ignored])
+    assert torch.allclose(acc[~ignored], base[~ignored] + dhc[~ignored], rtol=0, atol=1e-6)
+    hc.close()
+    hf.close()
+
+
 def test_partial_grads_path_matches_recompute(cuda):
     # Alg. 3/4 (fused_backward.hpp:162-202) == fused_backward_recompute
     H, W, Y = ob.make_instance(80, 48, 600, 13, -100, 0.25)
@@ -433,17 +467,18 @@ def test_simulated_vocab_parallel(cuda, ranks):
     check_grads(dh, dw, dH, dW, Y, ign)
 
 
-def test_native_vocab_parallel_single_rank(cuda):
+@pytest.mark.parametrize("frac", [0.0, 0.25])
+def test_native_vocab_parallel_single_rank(cuda, frac):
     """fce_vp_forward / fce_vp_backward over a 1-rank NCCL communicator."""
     import ctypes
     from paper_2511_17599_b200 import vocab_parallel as vp
-    H, W, Y, ign, st, rows, lred = _oracle_case(100, 32, 900, 9, 0.0, "mean")
+    H, W, Y, ign, st, rows, lred = _oracle_case(100, 32, 900, 9, frac, "mean")
     Hd, Wd, Yd = to_dev(H, W, Y)
     comm = vp.NativeComm.create_local(device=0)
-    out = vp.native_forward(comm, Hd, Wd, Yd, 0, 900, "mean")
+    out = vp.native_forward(comm, Hd, Wd, Yd, 0, 900, "mean", ign)
     check_forward(out, st, rows, lred, Y, ign, "mean")
-    dH, dW = ob.backward(H, W, Y, st, "mean")
-    dh, dw = vp.native_backward(comm, Hd, Wd, Yd, 0, 900, out.stats, "mean")
+    dH, dW = ob.backward(H, W, Y, st, "mean", 1.0, ign)
+    dh, dw = vp.native_backward(comm, Hd, Wd, Yd, 0, 900, out.stats, "mean", 1.0, ign)
     check_grads(dh, dw, dH, dW, Y, ign)
     comm.close()
 
