@@ -410,8 +410,9 @@ def main():
                    "parallelism": f"vocab-parallel x{world}" if comm is not None else "single GPU",
                    "l2": "inputs larger than L2 (W bf16 = %.2f GB)" % (v * d * 2 / 1e9)},
         "tflops_8ndv": flops_step / (ms_step / 1e3) / 1e12,
-        "pct_peak_step": flops_step / (ms_step / 1e3) / 1e12 / peaks["bf16_tflops"],
-        "pct_peak_step_sustained": flops_step / (ms_step / 1e3) / 1e12 / peak_sust,
+        # per-GPU fraction of the measured bf16 peak (whole-job flops / N GPUs)
+        "pct_peak_step": flops_step / (ms_step / 1e3) / 1e12 / peaks["bf16_tflops"] / world,
+        "pct_peak_step_sustained": flops_step / (ms_step / 1e3) / 1e12 / peak_sust / world,
         "model_tflops_6ndv": 6.0 * n * d * v / (ms_step / 1e3) / 1e12,
         "peak_hbm_bytes": int(peak_torch + ws_peak),
         "peak_hbm_breakdown": {"torch_inputs_outputs": int(peak_torch), "library_workspace": int(ws_peak)},

@@ -789,7 +789,18 @@ fce_status fce_backward(fce_handle h, const fce_problem* p, fce_stats stats, int
 
     // chunking of G = N_c x V_c bf16
     // defaults measured best on B200 at the Llama-3-8B shape
-    int64_t row_chunk = h->row_chunk ? h->row_chunk : 16384;
+    int64_t row_chunk = h->row_chunk;
+    if (!row_chunk && h->bwd_persistent) {
+        // As few row chunks as the G ring cap (1 GiB at kg = 1) allows, of equal
+        // size: every extra row chunk is another fp32 read-modify-write pass
+        // over dW (measured: Gemma-2-2B shape 213 -> 178 ms going from 4 chunks
+        // of 16384 to 1-2 chunks; profiles/r01_energy.md).
+        const int64_t band_guess = h->band_cols ? h->band_cols : 3072;
+        const int64_t cap = std::max<int64_t>(256, ((int64_t(1) << 30) / (2 * 2 * band_guess)) / 256 * 256);
+        row_chunk = ceil_div(n_k, ceil_div(n_k, cap));
+    } else if (!row_chunk) {
+        row_chunk = 16384;
+    }
     row_chunk = std::min(row_chunk, round_up(n_k, h->bwd_persistent ? 256 : kBM));
     if (h->bwd_persistent) row_chunk = round_up(row_chunk, 256);
     int64_t band = h->band_cols;

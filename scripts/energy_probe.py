@@ -17,11 +17,13 @@ ap.add_argument("--secs", type=float, default=3.0)
 ap.add_argument("--sets", nargs="*", default=[""])
 ap.add_argument("--shape", default="16384,4096,128256")
 ap.add_argument("--work", default="cublas,fwd,bwd,step")
+ap.add_argument("--ignore", type=float, default=0.0, help="fraction of ignore_index=-100 targets")
 a = ap.parse_args()
 nv.nvmlInit()
 dev = nv.nvmlDeviceGetHandleByIndex(int(os.environ.get("LOCAL_RANK", "0")))
 n, d, v = (int(x) for x in a.shape.split(","))
-H, W, Y = fce.generate_instance(n, d, v, 42)
+H, W, Y = fce.generate_instance(n, d, v, 42, -100, a.ignore)
+IGN = -100 if a.ignore > 0 else None
 dh = torch.empty(n, d, device="cuda")
 
 
@@ -83,15 +85,15 @@ for s in a.sets:
     for kv in filter(None, s.split(",")):
         k_, x = kv.split("=")
         h.set_option(k_, int(x))
-    out = fce.fused_forward(H, W, Y, "mean", handle=h)
+    out = fce.fused_forward(H, W, Y, "mean", IGN, handle=h)
     tag = s or "default"
     if "fwd" in work:
-        print(f"[{tag}] fwd  {measure(lambda: fce.fused_forward(H, W, Y, 'mean', handle=h), fl)}", flush=True)
+        print(f"[{tag}] fwd  {measure(lambda: fce.fused_forward(H, W, Y, 'mean', IGN, handle=h), fl)}", flush=True)
     if "bwd" in work:
-        print(f"[{tag}] bwd  {measure(lambda: fce.fused_backward_recompute(H, W, Y, out.stats, 'mean', 1.0, handle=h, dhidden=dh), 3 * fl)}", flush=True)
+        print(f"[{tag}] bwd  {measure(lambda: fce.fused_backward_recompute(H, W, Y, out.stats, 'mean', 1.0, IGN, handle=h, dhidden=dh), 3 * fl)}", flush=True)
     if "step" in work:
         def step():
-            o = fce.fused_forward(H, W, Y, "mean", handle=h)
+            o = fce.fused_forward(H, W, Y, "mean", IGN, handle=h)
             fce.fused_backward_recompute(H, W, Y, o.stats, "mean", 1.0, handle=h, dhidden=dh)
         print(f"[{tag}] step {measure(step, 4 * fl)}", flush=True)
     h.close()
