@@ -201,7 +201,7 @@ def main():
     ap.add_argument("--ref-rows", type=int, default=0, help="rows per reference step (0: one per host core, <= 16)")
     ap.add_argument("--ref-warmup", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--e2e-steps", type=int, default=6)
+    ap.add_argument("--e2e-steps", type=int, default=16)
     ap.add_argument("--force-vp", action="store_true",
                     help="use the native vocab-parallel (NCCL) path even on one rank (testing)")
     args = ap.parse_args()

@@ -443,6 +443,27 @@ def tp_rank_partial(hidden, weight_shard, v_offset: int, v_total: int, targets,
     return st
 
 
+def stream_stats(h_row, weight, target, lo: int, hi: int, handle=None) -> Stats:
+    """stream_stats (fused_forward.hpp:137-154): one hidden row over the vocabulary
+    range [lo, hi) -> 1-row Stats; the empty range is the identity."""
+    import torch
+    d = weight.shape[1]
+    if h_row.numel() != d:
+        raise DimensionMismatch(f"hidden length {h_row.numel()} != weight cols {d}")
+    if lo > hi or hi > weight.shape[0] or lo < 0:
+        raise DimensionMismatch(f"vocab range [{lo}, {hi}) not contained in [0, {weight.shape[0]})")
+    dev = weight.device
+    if lo == hi:
+        st = Stats.empty(1, dev)
+        st.m.fill_(float("-inf")); st.a.zero_(); st.z_target.zero_(); st.found.zero_()
+        return st
+    # a target outside the range (or none) never matches: use id hi
+    y = hi if target is None or target < 0 else int(target)
+    tv = torch.tensor([y], dtype=torch.int64, device=dev)
+    return tp_rank_partial(h_row.reshape(1, d), weight[lo:hi], lo, max(hi + 1, weight.shape[0] + 1), tv,
+                           None, handle)
+
+
 def merge_rank_partials(partials: Sequence[Stats], targets, reduction="mean", ignore_index=None,
                         handle=None):
     """Rank-ordered merge (parallel_sim.hpp:214-231) of partials -> FusedOutput."""

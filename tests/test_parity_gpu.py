@@ -243,6 +243,25 @@ def test_backward_dh_groups(cuda, kg):
     h.close()
 
 
+def test_stream_stats_ranges_merge_to_row_stats(cuda):
+    # stream_stats (fused_forward.hpp:137-154) over [0, k) and [k, V) merges to the row's stats
+    H, W, Y, ign, st, rows, lred = _oracle_case(4, 40, 700, 13, 0.0, "none")
+    Hd, Wd, Yd = to_dev(H, W, Y)
+    for r in range(4):
+        y = int(Y[r])
+        for k in (0, 1, y, y + 1, 350, 700):
+            parts = [fce.stream_stats(Hd[r], Wd, y, 0, k), fce.stream_stats(Hd[r], Wd, y, k, 700)]
+            out = fce.merge_rank_partials(parts, Yd[r:r + 1], "none")
+            assert int(out.stats.found.item()) == 1
+            assert abs(out.stats.m.item() - st["m"][r]) <= 1e-5 * max(1.0, abs(st["m"][r]))
+            assert abs(out.stats.a.item() - st["a"][r]) <= 1e-4 * st["a"][r]
+            assert abs(out.loss_rows.item() - rows[r]) <= LOSS_RTOL * max(1.0, abs(rows[r]))
+    empty = fce.stream_stats(Hd[0], Wd, None, 5, 5)
+    assert math.isinf(empty.m.item()) and empty.a.item() == 0 and empty.found.item() == 0
+    with pytest.raises(fce.DimensionMismatch):
+        fce.stream_stats(Hd[0], Wd, None, 5, 701)
+
+
 @pytest.mark.parametrize("window", [1, 3, 16, 128, 256, 257, 1000])
 def test_windowed_forward(cuda, window):
     # window sweep {1,3,16,128,256,257} (test_fused_forward.cpp:146-175)
