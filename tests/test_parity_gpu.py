@@ -415,6 +415,37 @@ def test_ignored_row_compaction_matches_full_rows(cuda, n, d, v, frac):
     hf.close()
 
 
+def test_cuda_graph_capture_replays_the_step(cuda):
+    """With validation off the forward + backward are stream-ordered with no host
+    sync, so a training step can be captured once and replayed as a CUDA graph."""
+    H, W, Y, ign, st, rows, lred = _oracle_case(300, 136, 1500, 17, 0.0, "mean")
+    Hd, Wd, Yd = to_dev(H, W, Y)
+    s = torch.cuda.Stream()
+    h = fce.Handle(0, s)
+    h.set_option("validate", 0)
+
+    def step():
+        out = fce.fused_forward(Hd, Wd, Yd, "mean", handle=h)
+        dh, dw = fce.fused_backward_recompute(Hd, Wd, Yd, out.stats, "mean", 1.0, handle=h)
+        return out.loss, dh, dw
+
+    s.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(s):
+        ref = step()  # warm: sizes the workspace outside the capture
+    torch.cuda.synchronize()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g, stream=s):
+        cap = step()
+    for t in cap:
+        t.zero_()
+    g.replay()
+    g.replay()
+    torch.cuda.synchronize()
+    assert torch.equal(cap[0], ref[0]) and torch.equal(cap[1], ref[1]) and torch.equal(cap[2], ref[2])
+    assert abs(cap[0].item() - lred) <= LOSS_RTOL * abs(lred)
+    h.close()
+
+
 def test_partial_grads_path_matches_recompute(cuda):
     # Alg. 3/4 (fused_backward.hpp:162-202) == fused_backward_recompute
     H, W, Y = ob.make_instance(80, 48, 600, 13, -100, 0.25)
