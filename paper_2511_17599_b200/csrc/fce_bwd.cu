@@ -534,9 +534,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(128 + 32 * kEpiWarps
                             fence_proxy_async_shared();
                             named_bar_sync(2 + grp, 128);
                             if (gl) {
-                                tma_store_2d(&maps.g_st, sbuf, un.gcol + un.n_tile * kBN + c64,
-                                             un.slot * static_cast<int>(p.nc_max) + un.m_blk * kPM +
-                                                 static_cast<int>(rank) * 128);
+                                tma_store_2d_hint(&maps.g_st, sbuf, un.gcol + un.n_tile * kBN + c64,
+                                                  un.slot * static_cast<int>(p.nc_max) + un.m_blk * kPM +
+                                                      static_cast<int>(rank) * 128,
+                                                  pol_gst);
                                 bulk_commit();
                             }
                         }
@@ -563,9 +564,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(128 + 32 * kEpiWarps
                             named_bar_sync(2 + grp, 128);
                             if (gl && !discard) {
                                 if (accumulate)
-                                    tma_reduce_add_2d(om, sbuf, un.n_tile * kBN + c32, orow);
+                                    tma_reduce_add_2d_hint(om, sbuf, un.n_tile * kBN + c32, orow, pol_out);
                                 else
-                                    tma_store_2d(om, sbuf, un.n_tile * kBN + c32, orow);
+                                    tma_store_2d_hint(om, sbuf, un.n_tile * kBN + c32, orow, pol_out);
                                 bulk_commit();
                             }
                         }
