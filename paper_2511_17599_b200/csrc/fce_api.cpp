@@ -805,9 +805,17 @@ fce_status fce_backward(fce_handle h, const fce_problem* p, fce_stats stats, int
     if (h->bwd_persistent) row_chunk = round_up(row_chunk, 256);
     int64_t band = h->band_cols;
     if (!band) {
-        // ~32 MB of G per chunk so it stays L2 resident between producer and consumers
-        band = h->bwd_persistent ? 3072
-                                 : std::max<int64_t>(kBN, ((int64_t(16) << 20) / row_chunk) / kBN * kBN);
+        if (h->bwd_persistent) {
+            // 3072 columns from 16384 rows up; shorter row chunks take wider bands
+            // (fewer dH passes, more units per phase): 3072 * sqrt(16384 / rows),
+            // to a multiple of 1024.  Measured best at 1024 / 4096 / 8192 /
+            // 16384 rows: 12288 / 6144 / 6144 / 3072-4096 (profiles/r01_band_small.log).
+            const double w = 3072.0 * std::sqrt(16384.0 / static_cast<double>(row_chunk));
+            band = std::max<int64_t>(3072, static_cast<int64_t>(std::llround(w / 1024.0)) * 1024);
+        } else {
+            // ~32 MB of G per chunk so it stays L2 resident between producer and consumers
+            band = std::max<int64_t>(kBN, ((int64_t(16) << 20) / row_chunk) / kBN * kBN);
+        }
     }
     band = std::min(band, round_up(p->v, kBN));
     // bands per dH group (persistent backward): dH is written once per group
