@@ -57,6 +57,7 @@ struct fce_handle_s {
     int64_t gemm_pair = 1;
     int64_t fwd_m_group = 0;  // forward raster: row blocks per L2 group (0 = default)
     int64_t fwd_pair = 0;     // forward on CTA pairs (fce_fwd_pair.cu); measured slower under the power cap
+    int64_t fwd_mc = 0;       // forward on 2-CTA clusters with W multicast
     int64_t bwd_unit_mask = 7;
     int64_t trace_ptr = 0;
     int64_t bwd_epi_warps = 8;
@@ -289,15 +290,16 @@ cudaEvent_t pool_event(fce_handle h) {
 // Launches one tile kernel; with timing on, brackets it with CUDA events on
 // the handle's stream and records its algorithmic flop count.
 cudaError_t timed_launch(fce_handle h, const TileParams& p, const TensorMaps& maps, double flops,
-                         bool fwd_pair = false) {
+                         int fwd_variant = 0) {
     cudaEvent_t e0 = nullptr, e1 = nullptr;
     if (h->timing) {
         e0 = pool_event(h);
         e1 = pool_event(h);
         cudaEventRecord(e0, h->stream);
     }
-    cudaError_t e = fwd_pair ? launch_fwd_pair(p, maps, h->sms, h->stream)
-                             : launch_tile_kernel(p, maps, h->sms, h->stream);
+    cudaError_t e = fwd_variant == 1   ? launch_fwd_pair(p, maps, h->sms, h->stream)
+                    : fwd_variant == 2 ? launch_fwd_mc(p, maps, h->sms, h->stream)
+                                       : launch_tile_kernel(p, maps, h->sms, h->stream);
     if (h->timing) {
         cudaEventRecord(e1, h->stream);
         h->pending.push_back({p.mode, e0, e1, flops});
@@ -324,6 +326,7 @@ void drain_timing(fce_handle h) {
 // split-V factor over the persistent grid (pairs count as one slot each).
 struct FwdGeom {
     bool pair;
+    bool mc;  // 2-CTA clusters with W multicast (cta_group::1 MMAs)
     int64_t m_blocks, v_tiles;
     int splits;
 };
@@ -331,9 +334,10 @@ struct FwdGeom {
 FwdGeom forward_geometry(fce_handle h, const fce_problem* p, int64_t window) {
     FwdGeom g;
     g.pair = h->fwd_pair != 0;
-    g.m_blocks = ceil_div(p->n, g.pair ? 256 : kBM);
+    g.mc = !g.pair && h->fwd_mc != 0;
+    g.m_blocks = ceil_div(p->n, (g.pair || g.mc) ? 256 : kBM);
     g.v_tiles = ceil_div(p->v, kBN);
-    g.splits = choose_splits(g.m_blocks, g.v_tiles, g.pair ? h->sms / 2 : h->sms, h->splits);
+    g.splits = choose_splits(g.m_blocks, g.v_tiles, (g.pair || g.mc) ? h->sms / 2 : h->sms, h->splits);
     if (window > 0) g.splits = static_cast<int>(std::min<int64_t>(g.v_tiles, ceil_div(p->v, window)));
     return g;
 }
@@ -345,7 +349,7 @@ fce_status run_forward_tiles(fce_handle h, const fce_problem* p, const FwdGeom& 
     TensorMaps maps;
     std::memset(&maps, 0, sizeof(maps));
     // pair: each CTA stages its 128 rows of H and its 128-row half of the W tile
-    const uint32_t b_box = g.pair ? 128 : kBN;
+    const uint32_t b_box = (g.pair || g.mc) ? 128 : kBN;
     if (!encode_map_2d(&maps.a0, p->hidden, p->d, p->n, p->ldh * 2, kBK, kBM) ||
         !encode_map_2d(&maps.b0, p->weight, p->d, p->v, p->ldw * 2, kBK, b_box))
         return fail(FCE_CUDA_ERROR, "cuTensorMapEncodeTiled failed for H / W");
@@ -355,7 +359,8 @@ fce_status run_forward_tiles(fce_handle h, const fce_problem* p, const FwdGeom& 
     tp.m_blocks = static_cast<int>(g.m_blocks);
     tp.v_tiles = static_cast<int>(g.v_tiles);
     tp.splits = g.splits;
-    tp.m_group = static_cast<int>(std::min<int64_t>(tp.m_blocks, h->fwd_m_group ? h->fwd_m_group : (g.pair ? 8 : 32)));
+    tp.m_group = static_cast<int>(
+        std::min<int64_t>(tp.m_blocks, h->fwd_m_group ? h->fwd_m_group : (g.pair ? 8 : g.mc ? 16 : 32)));
     tp.k_blocks = static_cast<int>(ceil_div(p->d, kBK));
     tp.units = tp.m_blocks * tp.splits;
     tp.targets = p->targets;
@@ -366,7 +371,7 @@ fce_status run_forward_tiles(fce_handle h, const fce_problem* p, const FwdGeom& 
     tp.part_a = pa;
     tp.part_zt = pzt;
     tp.part_found = pf;
-    cudaError_t e = timed_launch(h, tp, maps, 2.0 * p->n * p->d * p->v, g.pair);
+    cudaError_t e = timed_launch(h, tp, maps, 2.0 * p->n * p->d * p->v, g.pair ? 1 : g.mc ? 2 : 0);
     if (e != cudaSuccess) return fail(FCE_CUDA_ERROR, "forward tile kernel: %s", cudaGetErrorString(e));
     return FCE_OK;
 }
@@ -589,6 +594,8 @@ fce_status fce_set_option(fce_handle h, const char* key, int64_t value) {
         h->skip_ignored = value ? 1 : 0;
     } else if (!std::strcmp(key, "fwd_m_group")) {
         h->fwd_m_group = value;
+    } else if (!std::strcmp(key, "fwd_mc")) {
+        h->fwd_mc = value ? 1 : 0;
     } else if (!std::strcmp(key, "fwd_pair")) {
         h->fwd_pair = value ? 1 : 0;
     } else if (!std::strcmp(key, "gemm_pair")) {

@@ -101,6 +101,7 @@ struct BwdMaps {
 };
 
 cudaError_t launch_fwd_pair(const TileParams& p, const TensorMaps& maps, int sms, cudaStream_t stream);
+cudaError_t launch_fwd_mc(const TileParams& p, const TensorMaps& maps, int sms, cudaStream_t stream);
 
 cudaError_t launch_pair_gemm(const GemmProblem& q, const TensorMaps& maps, int sms,
                              cudaStream_t stream);

@@ -19,6 +19,7 @@
 // smem ring, warp 1 lane 0 issues tcgen05.mma (M=128, N=256, K=16) into one
 // of two TMEM accumulators (2 x 256 fp32 columns), warp 2 owns the TMEM
 // allocation, warps 4-7 drain TMEM with tcgen05.ld (thread = row).
+#include <algorithm>
 #include <cmath>
 #include <cstdio>
 #include <cudaTypedefs.h>
@@ -77,7 +78,11 @@ __device__ __forceinline__ Unit get_unit(const TileParams& p, int u) {
     return r;
 }
 
-template <int EPI>
+// MC (forward only): clusters of two CTAs on adjacent row blocks of the same
+// vocab tiles; each CTA loads its own H rows and one 128-row half of the W tile
+// and multicasts that half into both CTAs' stages, so every W byte leaves L2
+// once per pair.  Stage slots are released by both CTAs' MMA commits.
+template <int EPI, bool MC>
 __global__ void __launch_bounds__(kThreads, 1)
     fce_tile_kernel(const __grid_constant__ TileParams p, const __grid_constant__ TensorMaps maps) {
     extern __shared__ uint8_t smem_raw[];
@@ -94,11 +99,14 @@ __global__ void __launch_bounds__(kThreads, 1)
 
     const int warp = threadIdx.x >> 5;
     const int lane = threadIdx.x & 31;
+    const int rank = MC ? static_cast<int>(cluster_ctarank()) : 0;
+    const int u_first = MC ? static_cast<int>(blockIdx.x >> 1) : static_cast<int>(blockIdx.x);
+    const int u_step = MC ? static_cast<int>(gridDim.x >> 1) : static_cast<int>(gridDim.x);
 
     if (threadIdx.x == 0) {
         for (int s = 0; s < kStages; ++s) {
             mbar_init(&full[s], 1);
-            mbar_init(&empty[s], 1);
+            mbar_init(&empty[s], MC ? 2 : 1);
         }
         for (int b = 0; b < 2; ++b) {
             mbar_init(&tfull[b], 1);
@@ -118,7 +126,10 @@ __global__ void __launch_bounds__(kThreads, 1)
         tmem_alloc<512>(tmem_slot);
     }
     tc_fence_before();
-    __syncthreads();
+    if (MC)
+        cluster_sync_all();  // the peer multicasts into this CTA's stages / barriers
+    else
+        __syncthreads();
     tc_fence_after();
     const uint32_t tmem_base = *tmem_slot;
 
@@ -130,8 +141,9 @@ __global__ void __launch_bounds__(kThreads, 1)
             int stage = 0;
             uint32_t phase = 0;
             const uint32_t sa0 = smem_u32(sA), sb0 = smem_u32(sB);
-            for (int u = blockIdx.x; u < p.units; u += gridDim.x) {
-                const Unit un = get_unit(p, u);
+            for (int u = u_first; u < p.units; u += u_step) {
+                Unit un = get_unit(p, u);
+                if (MC) un.m_blk = 2 * un.m_blk + rank;
                 const CUtensorMap* ma = un.prob ? &maps.a1 : &maps.a0;
                 const CUtensorMap* mb = un.prob ? &maps.b1 : &maps.b0;
                 int kbs = p.k_blocks, a_mn = 0, b_mn = 0;
@@ -155,7 +167,10 @@ __global__ void __launch_bounds__(kThreads, 1)
                                 tma_load_2d_w(a_dst + j * 8192, ma, &full[stage], un.m_blk * kBM + 64 * j, kb * kBK,
                                               kEvictNormal);
                         }
-                        if (!b_mn) {
+                        if (MC) {
+                            tma_load_2d_mc_w(b_dst + rank * (kStageBytesB / 2), mb, &full[stage], kb * kBK,
+                                             n_tile * kBN + rank * (kBN / 2), 0x3, kEvictNormal);
+                        } else if (!b_mn) {
                             tma_load_2d_w(b_dst, mb, &full[stage], kb * kBK, n_tile * kBN, kEvictNormal);
                         } else {
 #pragma unroll
@@ -179,7 +194,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             int acc = 0;
             uint32_t acc_phase = 0;
             const uint32_t sa0 = smem_u32(sA), sb0 = smem_u32(sB);
-            for (int u = blockIdx.x; u < p.units; u += gridDim.x) {
+            for (int u = u_first; u < p.units; u += u_step) {
                 const Unit un = get_unit(p, u);
                 int kbs = p.k_blocks;
                 uint32_t a_mn = 0, b_mn = 0;
@@ -208,7 +223,10 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
                         for (int k = 0; k < kBK / 16; ++k)
                             umma_bf16_w(d_tmem, ads + k * astep, bds + k * bstep, idesc, (kb | k) != 0 ? 1u : 0u);
-                        umma_commit_w(&empty[stage]);
+                        if (MC)
+                            umma_commit_mc_w(&empty[stage], 0x3);
+                        else
+                            umma_commit_w(&empty[stage]);
                         if (++stage == kStages) {
                             stage = 0;
                             phase ^= 1;
@@ -226,8 +244,9 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int r = q * 32 + lane;
         int acc = 0;
         uint32_t acc_phase = 0;
-        for (int u = blockIdx.x; u < p.units; u += gridDim.x) {
-            const Unit un = get_unit(p, u);
+        for (int u = u_first; u < p.units; u += u_step) {
+            Unit un = get_unit(p, u);
+            if (MC) un.m_blk = 2 * un.m_blk + rank;
             const int64_t row = static_cast<int64_t>(un.m_blk) * kBM + r;
 
             // per-row state (forward / grad)
@@ -359,7 +378,10 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
 
     tc_fence_before();
-    __syncthreads();
+    if (MC)
+        cluster_sync_all();  // no CTA leaves while its peer may still signal it
+    else
+        __syncthreads();
     tc_fence_after();
     if (warp == 2) {
         tmem_dealloc<512>(tmem_base);
@@ -409,13 +431,40 @@ static cudaError_t launch_one(const TileParams& p, const TensorMaps& maps, int g
                               cudaStream_t stream) {
     static bool attr_done = false;
     if (!attr_done) {
-        cudaError_t e = cudaFuncSetAttribute(fce_tile_kernel<EPI>,
+        cudaError_t e = cudaFuncSetAttribute(fce_tile_kernel<EPI, false>,
                                              cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes);
         if (e != cudaSuccess) return e;
         attr_done = true;
     }
-    fce_tile_kernel<EPI><<<grid, kThreads, kSmemBytes, stream>>>(p, maps);
+    fce_tile_kernel<EPI, false><<<grid, kThreads, kSmemBytes, stream>>>(p, maps);
     return cudaGetLastError();
+}
+
+// Forward on 2-CTA clusters with W multicast (p.m_blocks counts row-block pairs).
+cudaError_t launch_fwd_mc(const TileParams& p, const TensorMaps& maps, int sms, cudaStream_t stream) {
+    if (p.units <= 0) return cudaSuccess;
+    static bool attr_done = false;
+    if (!attr_done) {
+        cudaError_t e = cudaFuncSetAttribute(fce_tile_kernel<kEpiForward, true>,
+                                             cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes);
+        if (e != cudaSuccess) return e;
+        attr_done = true;
+    }
+    int clusters = std::min(sms / 2, p.units);
+    if (clusters < 1) clusters = 1;
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(2 * clusters, 1, 1);
+    cfg.blockDim = dim3(kThreads, 1, 1);
+    cfg.dynamicSmemBytes = kSmemBytes;
+    cfg.stream = stream;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = 2;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, fce_tile_kernel<kEpiForward, true>, p, maps);
 }
 
 cudaError_t launch_tile_kernel(const TileParams& p, const TensorMaps& maps, int grid,

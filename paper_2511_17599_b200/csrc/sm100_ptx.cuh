@@ -484,5 +484,30 @@ __device__ __forceinline__ void tma_load_2d_w(uint32_t dst, const CUtensorMap* m
         "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "l"(policy)
         : "memory");
 }
+// cta_group::1 commit arriving on the barrier at the same offset in every CTA of mask
+__device__ __forceinline__ void umma_commit_mc_w(uint64_t* bar, uint16_t mask) {
+    asm volatile(
+        "{\n"
+        ".reg .pred e;\n"
+        "elect.sync _|e, 0xffffffff;\n"
+        "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;\n"
+        "}\n" ::"r"(smem_u32(bar)),
+        "h"(mask)
+        : "memory");
+}
+
+// TMA load multicast to the same smem offset (and barrier offset) in every CTA of mask
+__device__ __forceinline__ void tma_load_2d_mc_w(uint32_t dst, const CUtensorMap* map, uint64_t* bar, int32_t c0,
+                                                 int32_t c1, uint16_t mask, uint64_t policy) {
+    asm volatile(
+        "{\n"
+        ".reg .pred e;\n"
+        "elect.sync _|e, 0xffffffff;\n"
+        "@e cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes.multicast::cluster"
+        ".L2::cache_hint [%0], [%1, {%3, %4}], [%2], %5, %6;\n"
+        "}\n" ::"r"(dst),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "h"(mask), "l"(policy)
+        : "memory");
+}
 }  // namespace ptx
 }  // namespace fce

@@ -224,6 +224,23 @@ def test_forward_cta_pair_variant(cuda, shape):
     h.close()
 
 
+@pytest.mark.parametrize("shape", [(1, 8, 3), (129, 72, 511), (255, 72, 511), (257, 136, 3000),
+                                   (700, 4096, 1000), (1000, 64, 40000)])
+def test_forward_multicast_variant(cuda, shape):
+    """The 2-CTA-cluster forward with W multicast (option fwd_mc) against the
+    oracle, including an odd number of 128-row blocks (idle second CTA rows)."""
+    n, d, v = shape
+    H, W, Y, ign, st, rows, lred = _oracle_case(n, d, v, 29, 0.25, "mean")
+    Hd, Wd, Yd = to_dev(H, W, Y)
+    h = fce.Handle(0)
+    h.set_option("fwd_mc", 1)
+    out = fce.fused_forward(Hd, Wd, Yd, "mean", ign, handle=h)
+    check_forward(out, st, rows, lred, Y, ign, "mean")
+    ref = fce.fused_forward(Hd, Wd, Yd, "mean", ign)
+    assert abs(out.loss.item() - ref.loss.item()) <= 1e-6 * abs(ref.loss.item())
+    h.close()
+
+
 @pytest.mark.parametrize("kg", [1, 2, 3, 4, 8])
 def test_backward_dh_groups(cuda, kg):
     """dH contracted over groups of kg bands (ragged last group, short last row
