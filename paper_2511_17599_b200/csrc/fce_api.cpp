@@ -68,7 +68,7 @@ struct fce_handle_s {
     void* cws = nullptr;
     size_t cws_size = 0;
     int64_t launches = 0;
-    size_t bwd_scratch[4] = {0, 0, 0, 0};  // offsets of the persistent-backward scratch
+    size_t bwd_scratch[2] = {0, 0};  // workspace offsets of the G ring and the dependency counters
     // optional per-kernel CUDA-event timing of the tile kernels (bench roofline)
     int64_t timing = 0;
     struct Pending {
@@ -384,7 +384,7 @@ fce_status run_backward_persistent(fce_handle h, const fce_problem* p, const flo
                                    int accumulate_dhidden) {
     char* ws = static_cast<char*>(h->ws);
     __nv_bfloat16* g_ring = reinterpret_cast<__nv_bfloat16*>(ws + h->bwd_scratch[0]);
-    unsigned* d_ctr = reinterpret_cast<unsigned*>(ws + h->bwd_scratch[3]);
+    unsigned* d_ctr = reinterpret_cast<unsigned*>(ws + h->bwd_scratch[1]);
 
     const int64_t n_rc = ceil_div(p->n, row_chunk), n_bd = ceil_div(p->v, band);
     const int64_t n_chunks = n_rc * n_bd;
@@ -836,13 +836,10 @@ fce_status fce_backward(fce_handle h, const fce_problem* p, fce_stats stats, int
     const int64_t n_rc = ceil_div(n_k, row_chunk), n_bd = ceil_div(p->v, band);
     const int64_t n_chunks = n_rc * n_bd;
     const int64_t mb_max = ceil_div(row_chunk, 128);
-    const size_t o_tab = 0, o_bnd = 0;
     const size_t o_ctr = sc.take(sizeof(unsigned) * (1 + 4 * n_chunks + n_chunks * mb_max));
     if ((s = sc.commit())) return s;
     h->bwd_scratch[0] = o_G;
-    h->bwd_scratch[1] = o_tab;
-    h->bwd_scratch[2] = o_bnd;
-    h->bwd_scratch[3] = o_ctr;
+    h->bwd_scratch[1] = o_ctr;
     float* gamma = sc.ptr<float>(o_g);
     float* lse = sc.ptr<float>(o_l);
     __nv_bfloat16* G = sc.ptr<__nv_bfloat16>(o_G);
