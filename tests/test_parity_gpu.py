@@ -498,6 +498,50 @@ def test_concurrent_handles_on_two_streams(cuda):
         h.close()
 
 
+@pytest.mark.parametrize("pair", [0, 1])
+@pytest.mark.parametrize("a_mn,b_mn", [(0, 0), (0, 1), (1, 0), (1, 1)])
+def test_gemm_bf16_entry_matches_torch_fp32(cuda, pair, a_mn, b_mn):
+    """fce_gemm_bf16 (the tile kernels' generic contraction, exported for tests /
+    benchmarks): C = A . B^T against a torch fp32 matmul of the same bf16 values,
+    with ragged M, N, K and both operand majornesses; accumulate adds."""
+    g = torch.Generator(device="cuda").manual_seed(5 + 2 * a_mn + b_mn)
+    m, n, k = 333, 517, 200
+    A = torch.randn(m, k, device="cuda", generator=g).to(torch.bfloat16)
+    B = torch.randn(n, k, device="cuda", generator=g).to(torch.bfloat16)
+    ref = A.float() @ B.float().t()
+    a_in = A.t().contiguous() if a_mn else A
+    b_in = B.t().contiguous() if b_mn else B
+    h = fce.Handle(0)
+    h.set_option("gemm_pair", pair)
+    # the TMA maps need 16-byte rows: pad the stored leading dimension to a multiple of 8
+    def pad(x):
+        cols = x.shape[1]
+        buf = torch.zeros(x.shape[0], (cols + 7) // 8 * 8, dtype=x.dtype, device=x.device)
+        buf[:, :cols] = x
+        return buf[:, :cols]
+    out = fce.gemm_bf16(pad(a_in), pad(b_in), a_mn=bool(a_mn), b_mn=bool(b_mn), handle=h)
+    assert (out - ref).abs().max().item() <= 1e-4 * ref.abs().max().item()
+    out2 = fce.gemm_bf16(pad(a_in), pad(b_in), a_mn=bool(a_mn), b_mn=bool(b_mn), out=out.clone(),
+                         accumulate=True, handle=h)
+    assert (out2 - 2 * ref).abs().max().item() <= 2e-4 * ref.abs().max().item()
+    h.close()
+
+
+def test_non_persistent_backward_path(cuda):
+    """bwd_persistent = 0 (per-chunk G tile launch + dW/dH GEMM launch) against the oracle."""
+    H, W, Y, ign, st, rows, lred = _oracle_case(700, 136, 3000, 47, 0.25, "mean")
+    Hd, Wd, Yd = to_dev(H, W, Y)
+    h = fce.Handle(0)
+    h.set_option("bwd_persistent", 0)
+    h.set_option("row_chunk", 256)
+    h.set_option("band_cols", 1024)
+    out = fce.fused_forward(Hd, Wd, Yd, "mean", ign, handle=h)
+    dH, dW = ob.backward(H, W, Y, st, "mean", 1.0, ign)
+    dh, dw = fce.fused_backward_recompute(Hd, Wd, Yd, out.stats, "mean", 1.0, ign, handle=h)
+    check_grads(dh, dw, dH, dW, Y, ign)
+    h.close()
+
+
 def test_partial_grads_path_matches_recompute(cuda):
     # Alg. 3/4 (fused_backward.hpp:162-202) == fused_backward_recompute
     H, W, Y = ob.make_instance(80, 48, 600, 13, -100, 0.25)
