@@ -44,3 +44,35 @@ def test_no_nxv_allocation(cuda):
     assert ws < nxv / 8, (ws, nxv)
     assert extra - dh.numel() * 4 - dw.numel() * 4 < nxv / 8, (extra, nxv)
     h.close()
+
+
+def test_custom_op_registration_opcheck(cuda):
+    """fce::lce_forward / fce::lce_backward pass torch.library.opcheck (schema,
+    fake kernels, autograd registration)."""
+    from paper_2511_17599_b200.torch_op import lce_backward, lce_forward
+    H, W, Y = fce.generate_instance(200, 72, 900, 13, -100, 0.2)
+    H = H.clone().requires_grad_(True)
+    W = W.clone().requires_grad_(True)
+    torch.library.opcheck(lce_forward, (H, W, Y, 0, -100, True))
+    loss, m, a, z, f = lce_forward(H.detach(), W.detach(), Y, 0, -100, True)
+    torch.library.opcheck(lce_backward, (H.detach(), W.detach(), Y, m, a, z, f, torch.tensor(1.0, device="cuda"),
+                                         0, -100, True, True, True))
+
+
+def test_torch_compile_traces_the_op(cuda):
+    """A compiled training step keeps the op as one opaque call and matches eager."""
+    H, W, Y = fce.generate_instance(256, 128, 3000, 17, -100, 0.1)
+
+    def step(h, w, y):
+        return fused_linear_cross_entropy(h, w, y, "mean", -100) * 2.0
+
+    compiled = torch.compile(step, backend="aot_eager", fullgraph=True)
+    outs = []
+    for fn in (step, compiled):
+        h = H.clone().requires_grad_(True)
+        w = W.clone().requires_grad_(True)
+        loss = fn(h, w, Y)
+        loss.backward()
+        outs.append((loss.detach(), h.grad, w.grad))
+    for a, b in zip(*outs):
+        assert torch.equal(a, b)
