@@ -142,6 +142,24 @@ fce_status fce_backward(fce_handle h, const fce_problem* p, fce_stats stats, int
                         float upstream_scalar, const float* upstream_rows, float* dhidden,
                         int64_t lddh, float* dweight, int64_t lddw, int accumulate_dhidden);
 
+/* Element types of gradient outputs (fce_backward_ex). */
+typedef enum fce_dtype {
+    FCE_DTYPE_F32 = 0,
+    FCE_DTYPE_BF16 = 1
+} fce_dtype;
+
+/* fce_backward with the gradient element types chosen per output: FCE_DTYPE_F32
+ * (as fce_backward) or FCE_DTYPE_BF16 (round-to-nearest-even of the fp32 sums;
+ * the framework-facing form, e.g. a bf16 lm_head's .grad).  bf16 dW is written
+ * straight from the tensor-core accumulators when the backward runs in one row
+ * chunk (no fp32 V x D buffer at all); bf16 dH is accumulated in an fp32
+ * workspace across vocabulary bands and rounded once at the end.
+ * accumulate_dhidden requires an fp32 dH. */
+fce_status fce_backward_ex(fce_handle h, const fce_problem* p, fce_stats stats, int reduction,
+                           float upstream_scalar, const float* upstream_rows, void* dhidden,
+                           int64_t lddh, int dh_dtype, void* dweight, int64_t lddw, int dw_dtype,
+                           int accumulate_dhidden);
+
 /* The tile kernel's generic contraction (the dW / dH building block), exposed
  * for kernel-level tests and benchmarks: C[M, N] (+)= A . B^T in fp32 with bf16
  * operands; A is [M, K] (a_mn = 0, row stride lda) or stored as [K, M]

@@ -79,7 +79,7 @@ class FceStats(ctypes.Structure):
 EXPORTED_SYMBOLS = [
     "fce_create", "fce_destroy", "fce_set_stream", "fce_last_error", "fce_status_string",
     "fce_set_option", "fce_workspace_bytes", "fce_launch_count", "fce_kernel_stats", "fce_forward",
-    "fce_forward_partial", "fce_merge_partials", "fce_backward", "fce_gemm_bf16", "fce_scale",
+    "fce_forward_partial", "fce_merge_partials", "fce_backward", "fce_backward_ex", "fce_gemm_bf16", "fce_scale",
     "fce_generate_instance", "fce_f32_to_bf16",
     "fce_comm_unique_id", "fce_comm_init", "fce_comm_destroy", "fce_vp_last_error",
     "fce_vp_forward", "fce_vp_backward",
@@ -113,6 +113,8 @@ def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
         "fce_forward_partial": (I32, [P, ctypes.POINTER(FceProblem), FceStats]),
         "fce_merge_partials": (I32, [P, I32, I64, I64, P, P, P, P, P, I32, I64, I32, FceStats, P, P, P]),
         "fce_backward": (I32, [P, ctypes.POINTER(FceProblem), FceStats, I32, F, P, P, I64, P, I64, I32]),
+        "fce_backward_ex": (I32, [P, ctypes.POINTER(FceProblem), FceStats, I32, F, P, P, I64, I32, P, I64, I32,
+                                  I32]),
         "fce_scale": (I32, [P, P, I64, F]),
         "fce_gemm_bf16": (I32, [P, P, I64, I32, P, I64, I32, I64, I64, I64, P, I64, I32]),
         "fce_generate_instance": (I32, [P, I64, I64, I64, ctypes.c_uint64, P, I64, P, I64, P, I64, D, P, P]),
@@ -325,8 +327,10 @@ def fused_forward_windowed(hidden, weight, targets, window_size: int, reduction=
 def fused_backward_recompute(hidden, weight, targets, stats: Stats, reduction: str = "mean",
                              upstream=1.0, ignore_index=None, handle: Optional[Handle] = None,
                              want_dhidden: bool = True, want_dweight: bool = True,
-                             dhidden=None, accumulate_dhidden: bool = False):
-    """Backward by logit recompute (fused_backward.hpp:118-140) -> (dH, dW) fp32."""
+                             dhidden=None, accumulate_dhidden: bool = False, grad_dtype=None):
+    """Backward by logit recompute (fused_backward.hpp:118-140) -> (dH, dW), fp32
+    by default; grad_dtype=torch.bfloat16 returns bf16 gradients (fce_backward_ex:
+    dW rounded straight from the accumulators, no fp32 V x D buffer)."""
     import torch
     if reduction not in REDUCTIONS:
         raise UnsupportedReduction(reduction)
@@ -339,13 +343,24 @@ def fused_backward_recompute(hidden, weight, targets, stats: Stats, reduction: s
         up_scalar = float(upstream)
     else:
         up_rows = upstream.to(device=dev, dtype=torch.float32).contiguous()
+    gdt = torch.float32 if grad_dtype is None else grad_dtype
+    if gdt not in (torch.float32, torch.bfloat16):
+        raise InvalidArgument("grad_dtype must be torch.float32 or torch.bfloat16")
     if dhidden is None and want_dhidden:
-        dhidden = torch.empty(p.n, p.d, dtype=torch.float32, device=dev)
-    dweight = torch.empty(p.v, p.d, dtype=torch.float32, device=dev) if want_dweight else None
-    _check(h.lib.fce_backward(h.raw, ctypes.byref(p), stats.c(), REDUCTIONS[reduction], up_scalar,
-                              _ptr(up_rows), _ptr(dhidden), dhidden.stride(0) if dhidden is not None else 0,
-                              _ptr(dweight), dweight.stride(0) if dweight is not None else 0,
-                              1 if accumulate_dhidden else 0))
+        dhidden = torch.empty(p.n, p.d, dtype=gdt, device=dev)
+    dweight = torch.empty(p.v, p.d, dtype=gdt, device=dev) if want_dweight else None
+    if gdt == torch.float32 and (dhidden is None or dhidden.dtype == torch.float32):
+        _check(h.lib.fce_backward(h.raw, ctypes.byref(p), stats.c(), REDUCTIONS[reduction], up_scalar,
+                                  _ptr(up_rows), _ptr(dhidden), dhidden.stride(0) if dhidden is not None else 0,
+                                  _ptr(dweight), dweight.stride(0) if dweight is not None else 0,
+                                  1 if accumulate_dhidden else 0))
+    else:
+        code = {torch.float32: 0, torch.bfloat16: 1}
+        _check(h.lib.fce_backward_ex(h.raw, ctypes.byref(p), stats.c(), REDUCTIONS[reduction], up_scalar,
+                                     _ptr(up_rows), _ptr(dhidden), dhidden.stride(0) if dhidden is not None else 0,
+                                     code[dhidden.dtype] if dhidden is not None else 0,
+                                     _ptr(dweight), dweight.stride(0) if dweight is not None else 0,
+                                     code[gdt], 1 if accumulate_dhidden else 0))
     return dhidden, dweight
 
 

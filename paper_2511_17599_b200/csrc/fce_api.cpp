@@ -381,7 +381,7 @@ fce_status run_forward_tiles(fce_handle h, const fce_problem* p, const FwdGeom& 
 fce_status run_backward_persistent(fce_handle h, const fce_problem* p, const float* gamma,
                                    const float* lse, int64_t row_chunk, int64_t band, int kg,
                                    float* dhidden, int64_t lddh, float* dweight, int64_t lddw,
-                                   int accumulate_dhidden) {
+                                   int accumulate_dhidden, bool dw_bf16 = false) {
     char* ws = static_cast<char*>(h->ws);
     __nv_bfloat16* g_ring = reinterpret_cast<__nv_bfloat16*>(ws + h->bwd_scratch[0]);
     unsigned* d_ctr = reinterpret_cast<unsigned*>(ws + h->bwd_scratch[1]);
@@ -418,6 +418,7 @@ fce_status run_backward_persistent(fce_handle h, const fce_problem* p, const flo
     bp.l2_hints = static_cast<int>(h->l2_hints);
     bp.unit_mask = static_cast<int>(h->bwd_unit_mask);
     bp.epi_warps = static_cast<int>(h->bwd_epi_warps);
+    bp.dw_bf16 = dw_bf16 ? 1 : 0;
     bp.trace = reinterpret_cast<unsigned long long*>(h->trace_ptr);
     bp.nc_max = row_chunk;
     bp.ldg = band;
@@ -463,9 +464,13 @@ fce_status run_backward_persistent(fce_handle h, const fce_problem* p, const flo
     if (h->bwd_tma_epi) {
         bool ok = encode_map_2d(&maps.g_st, g_ring, bp.ldr, ring_rows, bp.ldr * 2, 64, 128);
         if (ok && dhidden) ok = encode_map_2d(&maps.dh_st, dhidden, p->d, p->n, lddh * 4, 32, 128, true);
-        if (ok && dweight) ok = encode_map_2d(&maps.dw_st, dweight, p->d, p->v, lddw * 4, 32, 128, true);
+        if (ok && dweight)
+            ok = dw_bf16 ? encode_map_2d(&maps.dw_st, dweight, p->d, p->v, lddw * 2, 64, 128)
+                         : encode_map_2d(&maps.dw_st, dweight, p->d, p->v, lddw * 4, 32, 128, true);
         bp.tma_epi = ok ? 1 : 0;
     }
+    if (dw_bf16 && !bp.tma_epi)
+        return fail(FCE_CUDA_ERROR, "bf16 dW needs the TMA epilogue (16-byte aligned rows)");
     cudaEvent_t e0 = nullptr, e1 = nullptr;
     if (h->timing) {
         e0 = pool_event(h);
@@ -768,9 +773,27 @@ static fce_status run_backward_tiles(fce_handle h, const fce_problem* p, const f
 fce_status fce_backward(fce_handle h, const fce_problem* p, fce_stats stats, int reduction,
                         float upstream_scalar, const float* upstream_rows, float* dhidden,
                         int64_t lddh, float* dweight, int64_t lddw, int accumulate_dhidden) {
+    return fce_backward_ex(h, p, stats, reduction, upstream_scalar, upstream_rows, dhidden, lddh, FCE_DTYPE_F32,
+                           dweight, lddw, FCE_DTYPE_F32, accumulate_dhidden);
+}
+
+fce_status fce_backward_ex(fce_handle h, const fce_problem* p, fce_stats stats, int reduction,
+                           float upstream_scalar, const float* upstream_rows, void* dhidden_out,
+                           int64_t lddh, int dh_dtype, void* dweight_out, int64_t lddw, int dw_dtype,
+                           int accumulate_dhidden) {
     fce_status s = check_handle(h);
     if (s) return s;
     if ((s = check_problem(p))) return s;
+    if ((dh_dtype != FCE_DTYPE_F32 && dh_dtype != FCE_DTYPE_BF16) ||
+        (dw_dtype != FCE_DTYPE_F32 && dw_dtype != FCE_DTYPE_BF16))
+        return fail(FCE_INVALID_ARGUMENT, "gradient dtype must be FCE_DTYPE_F32 or FCE_DTYPE_BF16");
+    if (dh_dtype == FCE_DTYPE_BF16 && accumulate_dhidden)
+        return fail(FCE_INVALID_ARGUMENT, "accumulate_dhidden requires an fp32 dH");
+    const bool dh_bf16 = dhidden_out && dh_dtype == FCE_DTYPE_BF16;
+    const bool dw_bf16 = dweight_out && dw_dtype == FCE_DTYPE_BF16;
+    // fp32 views; bf16 outputs are redirected below
+    float* dhidden = dh_bf16 ? nullptr : static_cast<float*>(dhidden_out);
+    float* dweight = dw_bf16 ? nullptr : static_cast<float*>(dweight_out);
     if (reduction < 0 || reduction > 2) return fail(FCE_UNSUPPORTED_REDUCTION, "unknown reduction %d", reduction);
     if (reduction == FCE_REDUCTION_NONE && !upstream_rows)
         return fail(FCE_INCONSISTENT_UPSTREAM, "reduction none requires a per-position upstream gradient");
@@ -778,8 +801,8 @@ fce_status fce_backward(fce_handle h, const fce_problem* p, fce_stats stats, int
         return fail(FCE_INCONSISTENT_UPSTREAM, "scalar reductions require a scalar upstream gradient");
     if (!stats.m || !stats.a || !stats.found)
         return fail(FCE_MISSING_STATS, "stats cache (m, a, found) is required");
-    if (dhidden && lddh < p->d) return fail(FCE_DIMENSION_MISMATCH, "lddh < d");
-    if (dweight && lddw < p->d) return fail(FCE_DIMENSION_MISMATCH, "lddw < d");
+    if (dhidden_out && lddh < p->d) return fail(FCE_DIMENSION_MISMATCH, "lddh < d");
+    if (dweight_out && lddw < p->d) return fail(FCE_DIMENSION_MISMATCH, "lddw < d");
     const int64_t v_total = p->v_total ? p->v_total : p->v;
 
     if ((s = reset_flags(h))) return s;
@@ -790,7 +813,7 @@ fce_status fce_backward(fce_handle h, const fce_problem* p, fce_stats stats, int
     // ignored rows compacted away (their gradient rows are exactly zero)
     Compact cp;
     fce_problem pcv;
-    if ((s = plan_compaction(h, p, true, dhidden != nullptr, &cp, &pcv))) return s;
+    if ((s = plan_compaction(h, p, true, dhidden_out != nullptr, &cp, &pcv))) return s;
     const fce_problem* pk = &pcv;  // the problem the tile kernels see
     const int64_t n_k = std::max<int64_t>(pk->n, 1);
 
@@ -837,19 +860,40 @@ fce_status fce_backward(fce_handle h, const fce_problem* p, fce_stats stats, int
     const int64_t n_chunks = n_rc * n_bd;
     const int64_t mb_max = ceil_div(row_chunk, 128);
     const size_t o_ctr = sc.take(sizeof(unsigned) * (1 + 4 * n_chunks + n_chunks * mb_max));
+    // bf16 outputs: dH is summed in fp32 over the bands (workspace, rounded at the
+    // end); dW goes out as bf16 straight from the accumulators when it is written
+    // once (persistent backward, one row chunk, TMA epilogue), else via fp32
+    const int64_t ld32 = round_up(p->d, 4);
+    const bool dw_direct = dw_bf16 && h->bwd_persistent && n_rc == 1 && h->bwd_tma_epi && lddw % 8 == 0 &&
+                           aligned16(dweight_out);
+    const size_t o_dhf = dh_bf16 ? sc.take(sizeof(float) * p->n * ld32) : 0;
+    const size_t o_dwf = (dw_bf16 && !dw_direct) ? sc.take(sizeof(float) * p->v * ld32) : 0;
     if ((s = sc.commit())) return s;
     h->bwd_scratch[0] = o_G;
     h->bwd_scratch[1] = o_ctr;
     float* gamma = sc.ptr<float>(o_g);
     float* lse = sc.ptr<float>(o_l);
     __nv_bfloat16* G = sc.ptr<__nv_bfloat16>(o_G);
+    const int64_t lddh_out = lddh;  // caller's dH leading dimension (bf16 output)
+    if (dh_bf16) {
+        dhidden = sc.ptr<float>(o_dhf);
+        lddh = ld32;
+    }
+    float* dw_store = dweight;  // what the kernels write (fp32, or bf16 reinterpreted)
+    int64_t lddw_k = lddw;
+    if (dw_bf16 && dw_direct) {
+        dw_store = static_cast<float*>(dweight_out);
+    } else if (dw_bf16) {
+        dw_store = sc.ptr<float>(o_dwf);
+        lddw_k = ld32;
+    }
 
     e = launch_gamma(p->n, p->targets, p->has_ignore, p->ignore_index, stats.m, stats.a, stats.found,
                      reduction, upstream_scalar, upstream_rows, h->count, gamma, lse, h->err, h->stream);
     if (e != cudaSuccess) return fail(FCE_CUDA_ERROR, "gamma kernel: %s", cudaGetErrorString(e));
     h->launches += 1;
     if ((s = read_errors(h, h->validate != 0))) return s;
-    if (!dhidden && !dweight) return FCE_OK;
+    if (!dhidden && !dw_store) return FCE_OK;
 
     float* dh_k = dhidden;
     int64_t lddh_k = lddh;
@@ -864,17 +908,18 @@ fce_status fce_backward(fce_handle h, const fce_problem* p, fce_stats stats, int
         dh_k = cp.dh;
         lddh_k = cp.lddh;
         acc_k = 0;
-        if (cp.n_valid == 0 && dweight) {
+        if (cp.n_valid == 0 && dw_store) {
             // nothing valid: dW is exactly zero (zero-initialised, never accumulated)
-            FCE_CUDA(cudaMemset2DAsync(dweight, lddw * sizeof(float), 0, p->d * sizeof(float), p->v, h->stream));
+            const size_t es = dw_direct ? sizeof(__nv_bfloat16) : sizeof(float);
+            FCE_CUDA(cudaMemset2DAsync(dw_store, lddw_k * es, 0, p->d * es, p->v, h->stream));
         }
     }
     if (pk->n > 0) {
         if (h->bwd_persistent) {
-            s = run_backward_persistent(h, pk, gamma, lse, row_chunk, band, kg, dh_k, lddh_k, dweight,
-                                        lddw, acc_k);
+            s = run_backward_persistent(h, pk, gamma, lse, row_chunk, band, kg, dh_k, lddh_k, dw_store,
+                                        lddw_k, acc_k, dw_direct);
         } else {
-            s = run_backward_tiles(h, pk, gamma, lse, row_chunk, band, G, dh_k, lddh_k, dweight, lddw,
+            s = run_backward_tiles(h, pk, gamma, lse, row_chunk, band, G, dh_k, lddh_k, dw_store, lddw_k,
                                    acc_k);
         }
         if (s) return s;
@@ -883,6 +928,18 @@ fce_status fce_backward(fce_handle h, const fce_problem* p, fce_stats stats, int
         e = launch_scatter_rows_f32(cp.dh, cp.lddh, dhidden, lddh, p->d, cp.map, p->n, accumulate_dhidden,
                                     h->stream);
         if (e != cudaSuccess) return fail(FCE_CUDA_ERROR, "scatter kernel: %s", cudaGetErrorString(e));
+        h->launches += 1;
+    }
+    if (dh_bf16) {
+        e = launch_round_to_bf16(dhidden, p->n, p->d, lddh, static_cast<__nv_bfloat16*>(dhidden_out), lddh_out,
+                                 h->stream);
+        if (e != cudaSuccess) return fail(FCE_CUDA_ERROR, "bf16 rounding: %s", cudaGetErrorString(e));
+        h->launches += 1;
+    }
+    if (dw_bf16 && !dw_direct) {
+        e = launch_round_to_bf16(dw_store, p->v, p->d, lddw_k, static_cast<__nv_bfloat16*>(dweight_out), lddw,
+                                 h->stream);
+        if (e != cudaSuccess) return fail(FCE_CUDA_ERROR, "bf16 rounding: %s", cudaGetErrorString(e));
         h->launches += 1;
     }
     return FCE_OK;

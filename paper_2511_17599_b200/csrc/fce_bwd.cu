@@ -541,6 +541,35 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(128 + 32 * kEpiWarps
                                 bulk_commit();
                             }
                         }
+                    } else if (un.type == kUnitDW && p.dw_bf16) {
+                        // bf16 dW (one row chunk: written exactly once): 64-column
+                        // slices of RNE-rounded pairs, 128-byte rows through TMA
+                        const int orow = un.vb + un.m_blk * kPM + static_cast<int>(rank) * 128;
+                        const bool discard = ((p.unit_mask >> 5) & 1) || ((p.unit_mask >> 7) & 1);
+#pragma unroll 1
+                        for (int sl = 0; sl < ncols / 64; ++sl) {
+                            const int c64 = gcol0 + sl * 64;
+                            if (gl) bulk_wait_read0();
+                            named_bar_sync(2 + grp, 128);
+                            uint32_t packed[32];
+#pragma unroll
+                            for (int h2 = 0; h2 < 2; ++h2) {
+                                float v[32];
+                                tmem_ld32(taddr + c64 + h2 * 32, v);
+#pragma unroll
+                                for (int j = 0; j < 32; j += 2) packed[h2 * 16 + (j >> 1)] = pack_bf16(v[j], v[j + 1]);
+                            }
+#pragma unroll
+                            for (int ch = 0; ch < 8; ++ch)
+                                st_shared_v4(my_row + ((static_cast<uint32_t>(ch) ^ sw) << 4), packed[4 * ch],
+                                             packed[4 * ch + 1], packed[4 * ch + 2], packed[4 * ch + 3]);
+                            fence_proxy_async_shared();
+                            named_bar_sync(2 + grp, 128);
+                            if (gl && !discard) {
+                                tma_store_2d_hint(&maps.dw_st, sbuf, un.n_tile * kBN + c64, orow, pol_out);
+                                bulk_commit();
+                            }
+                        }
                     } else {
                         const bool is_dh = un.type == kUnitDH;
                         const bool accumulate = is_dh ? (un.gl > 0 || p.accumulate_dh) : (un.row_idx > 0);

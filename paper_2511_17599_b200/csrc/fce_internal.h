@@ -81,6 +81,7 @@ struct BwdParams {
     int unit_mask;           // debug / profiling: bit0 grad, bit1 dH, bit2 dW units do work
     int epi_warps;           // 4 or 8 epilogue warps per CTA
     int tma_epi;             // 1: epilogue writes G / dH / dW through SMEM + TMA store / reduce-add
+    int dw_bf16;             // 1: dW is bf16 (one row chunk, stored once from the accumulators)
     int l2_hints;            // bit0: evict_first on dH/dW writes, bit1: evict_last on G loads,
                              // bit2: evict_last on G stores, bit3: evict_first on H loads (dW)
     int64_t nc_max, ldg, ldr, d, lddh, lddw, v_offset, ignore_index;  // ldg = band, ldr = kg * band
@@ -92,7 +93,7 @@ struct BwdParams {
     const float* gamma;
     __nv_bfloat16* g_ring;   // [2 group slots][nc_max][ldr]: band j of a group at column j * ldg
     float* dh;
-    float* dw;
+    float* dw;               // fp32 dW, or the bf16 dW (reinterpreted) when dw_bf16
 };
 
 struct BwdMaps {
@@ -131,6 +132,8 @@ cudaError_t launch_merge_stats(int parts, int64_t n, int64_t part_stride, const 
                                int emit_loss, float* m, float* a, float* zt, uint8_t* found,
                                float* lse, float* loss_rows, double* block_sums, int* err_flags,
                                cudaStream_t stream, int* blocks_out, const int* row_map = nullptr);
+cudaError_t launch_round_to_bf16(const float* in, int64_t rows, int64_t cols, int64_t ld_in,
+                                 __nv_bfloat16* out, int64_t ld_out, cudaStream_t stream);
 // ignored-row compaction (fce_kernels.cu)
 cudaError_t launch_row_map(const int64_t* targets, int64_t n, int64_t ignore_index, int* row_map,
                            int* rows, cudaStream_t stream);

@@ -886,6 +886,24 @@ __global__ void k_f32_to_bf16(const float* __restrict__ in, int64_t rows, int64_
     }
 }
 
+// out[r, c] = bf16_rn(in[r, c]) for c < cols (padding columns untouched)
+__global__ void k_round_to_bf16(const float* __restrict__ in, int64_t rows, int64_t cols, int64_t ld_in,
+                                __nv_bfloat16* out, int64_t ld_out) {
+    const int64_t total = rows * cols;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t r = i / cols, c = i - r * cols;
+        out[r * ld_out + c] = __float2bfloat16_rn(in[r * ld_in + c]);
+    }
+}
+
+cudaError_t launch_round_to_bf16(const float* in, int64_t rows, int64_t cols, int64_t ld_in,
+                                 __nv_bfloat16* out, int64_t ld_out, cudaStream_t stream) {
+    if (rows <= 0 || cols <= 0) return cudaSuccess;
+    k_round_to_bf16<<<148 * 8, 256, 0, stream>>>(in, rows, cols, ld_in, out, ld_out);
+    return cudaGetLastError();
+}
+
 cudaError_t launch_f32_to_bf16(const float* in, int64_t rows, int64_t cols, int64_t ld_in,
                                __nv_bfloat16* out, int64_t ld_out, int* err_flags,
                                cudaStream_t stream) {

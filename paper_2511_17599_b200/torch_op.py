@@ -56,10 +56,13 @@ def lce_backward(hidden: torch.Tensor, weight: torch.Tensor, targets: torch.Tens
         upstream = grad_out.float().contiguous()
     else:
         upstream = float(grad_out.item())
+    # gradients come out of the library in the parameters' dtype (bf16 dW is
+    # rounded straight from the tensor-core accumulators)
+    gdt = torch.bfloat16 if weight.dtype == torch.bfloat16 else torch.float32
     dh, dw = fce.fused_backward_recompute(hidden, weight, targets, stats, _RED_NAME[reduction], upstream,
                                           ignore_index if has_ignore else None,
                                           want_dhidden=want_dhidden or not want_dweight,
-                                          want_dweight=want_dweight)
+                                          want_dweight=want_dweight, grad_dtype=gdt)
     dh = dh.to(hidden.dtype) if (want_dhidden and dh is not None) else hidden.new_empty((0,))
     dw = dw.to(weight.dtype) if (want_dweight and dw is not None) else weight.new_empty((0,))
     return dh, dw

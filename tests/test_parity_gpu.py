@@ -542,6 +542,33 @@ def test_non_persistent_backward_path(cuda):
     h.close()
 
 
+@pytest.mark.parametrize("opts,frac", [({}, 0.0), ({}, 0.25), ({"row_chunk": 256}, 0.0),
+                                       ({"bwd_persistent": 0, "row_chunk": 256, "band_cols": 1024}, 0.25)])
+def test_bf16_gradient_outputs(cuda, opts, frac):
+    """fce_backward_ex with bf16 dH / dW equals the fp32 gradients rounded to
+    bf16 (direct bf16 dW epilogue with one row chunk; fp32 workspace + rounding
+    otherwise), and stays within the oracle tolerance."""
+    H, W, Y, ign, st, rows, lred = _oracle_case(700, 136, 3000, 53, frac, "mean")
+    Hd, Wd, Yd = to_dev(H, W, Y)
+    h = fce.Handle(0)
+    for k, v in opts.items():
+        h.set_option(k, v)
+    out = fce.fused_forward(Hd, Wd, Yd, "mean", ign, handle=h)
+    dh32, dw32 = fce.fused_backward_recompute(Hd, Wd, Yd, out.stats, "mean", 1.0, ign, handle=h)
+    dh16, dw16 = fce.fused_backward_recompute(Hd, Wd, Yd, out.stats, "mean", 1.0, ign, handle=h,
+                                              grad_dtype=torch.bfloat16)
+    assert dh16.dtype == torch.bfloat16 and dw16.dtype == torch.bfloat16
+    assert torch.equal(dh16, dh32.to(torch.bfloat16))
+    assert torch.equal(dw16, dw32.to(torch.bfloat16))
+    dH, dW = ob.backward(H, W, Y, st, "mean", 1.0, ign)
+    check_grads(dh16.float(), dw16.float(), dH, dW, Y, ign)
+    with pytest.raises(fce.InvalidArgument):
+        fce.fused_backward_recompute(Hd, Wd, Yd, out.stats, "mean", 1.0, ign, handle=h,
+                                     dhidden=torch.zeros_like(dh16), accumulate_dhidden=True,
+                                     grad_dtype=torch.bfloat16)
+    h.close()
+
+
 def test_partial_grads_path_matches_recompute(cuda):
     # Alg. 3/4 (fused_backward.hpp:162-202) == fused_backward_recompute
     H, W, Y = ob.make_instance(80, 48, 600, 13, -100, 0.25)
