@@ -80,3 +80,35 @@ def test_sass_is_tcgen05():
     out = subprocess.run(["cuobjdump", "-sass", fce.LIB_PATH], capture_output=True, text=True).stdout
     assert "UTCHMMA" in out and "UTMALDG" in out and "LDTM" in out
     assert not re.search(r"\bHMMA\b", out)
+
+
+def test_headers_are_plain_c_and_link(tmp_path):
+    """The boundary is a C ABI: include/fce/*.h compile as C11 (no C++ types)
+    and a C program links against libfce.so and calls it (without a GPU it
+    gets FCE_CUDA_ERROR, never a CPU result)."""
+    import subprocess
+    src = tmp_path / "abi.c"
+    src.write_text(r'''
+#include <stdio.h>
+#include "fce/fce.h"
+#include "fce/fce_vp.h"
+int main(void) {
+    fce_handle h = 0;
+    fce_status s = fce_create(&h, 0, NULL);
+    printf("%d %s\n", (int)s, fce_status_string(FCE_DIMENSION_MISMATCH));
+    if (s == FCE_OK) fce_destroy(h);
+    return 0;
+}
+''')
+    exe = tmp_path / "abi"
+    lib_dir = os.path.join(ROOT, "paper_2511_17599_b200")
+    r = subprocess.run(["gcc", "-std=c11", "-Wall", "-Werror", "-I", os.path.join(ROOT, "include"),
+                        "-I", "/usr/local/cuda/include", str(src), "-o", str(exe), "-L", lib_dir, "-lfce",
+                        f"-Wl,-rpath,{lib_dir}"], capture_output=True, text=True)
+    assert r.returncode == 0, r.stderr
+    r = subprocess.run([str(exe)], capture_output=True, text=True, timeout=120)
+    assert r.returncode == 0, r.stderr
+    code, name = r.stdout.split()
+    assert name == "DimensionMismatch"
+    import torch
+    assert int(code) == (0 if torch.cuda.is_available() else 100)
