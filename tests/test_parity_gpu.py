@@ -170,7 +170,7 @@ def test_random_ragged_shapes(cuda, rep):
     check_grads(dh, dw, dH, dW, Y, ign)
 
 
-@pytest.mark.parametrize("shape", [(1, 1, 1), (1, 8, 1), (3, 1, 2), (128, 64, 256), (129, 64, 257),
+@pytest.mark.parametrize("shape", [(1, 1, 1), (1, 8, 1), (3, 1, 2), (128, 64, 256), (129, 64, 257), (300, 16384, 1000), (3, 12288, 70000),
                                    (255, 72, 511), (256, 128, 513), (384, 4096, 300)])
 def test_tile_edges(cuda, shape):
     n, d, v = shape
