@@ -47,3 +47,33 @@ def test_random_case(cuda, case):
     dh, dw = fce.fused_backward_recompute(Hd, Wd, Yd, out.stats, red, upd, ign, handle=h)
     check_grads(dh, dw, dH, dW, Y, ign)
     h.close()
+
+
+@pytest.mark.parametrize("case", range(30))
+def test_random_vocab_parallel_case(cuda, case):
+    """Simulated vocabulary-parallel ranks (tp_rank_partial / rank-ordered merge /
+    per-shard backward summed into dH) on random shapes, shard counts, ignore
+    fractions and windows, against the oracle."""
+    from test_parity_gpu import _tp_backward
+    rng = np.random.default_rng(9000 + case)
+    n = int(rng.integers(1, 700))
+    d = int(rng.integers(1, 200))
+    v = int(rng.integers(2, 3000))
+    ranks = int(rng.integers(2, min(9, v + 1)))
+    frac = [0.0, 0.4][case % 2]
+    red = ["mean", "sum"][(case // 2) % 2]
+    H, W, Y = ob.make_instance(n, d, v, 300 + case, -100, frac)
+    ign = -100 if frac > 0 else None
+    st, rows, lred = ob.forward(H, W, Y, red, ign)
+    Hd, Wd, Yd = to_dev(H, W, Y)
+    parts = [fce.tp_rank_partial(Hd, Wd[lo:hi], lo, v, Yd, ign) for lo, hi in fce.shard_ranges(v, ranks)]
+    out = fce.merge_rank_partials(parts, Yd, red, ign)
+    check_forward(out, st, rows, lred, Y, ign, red)
+    dH, dW = ob.backward(H, W, Y, st, red, 1.0, ign)
+    dh, dw = _tp_backward(Hd, Wd, Yd, out.stats, red, 1.0, ign, ranks)
+    check_grads(dh, dw, dH, dW, Y, ign)
+    if case % 3 == 0:
+        window = int(rng.integers(1, v + 1))
+        stw, rowsw, lredw = ob.forward(H, W, Y, red, ign, window)
+        outw = fce.fused_forward_windowed(Hd, Wd, Yd, window, red, ign)
+        check_forward(outw, stw, rowsw, lredw, Y, ign, red)
