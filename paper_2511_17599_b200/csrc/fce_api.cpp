@@ -186,20 +186,21 @@ fce_status reset_flags(fce_handle h) {
 
 // Ignored-row compaction (the reference skips ignored positions outright,
 // fused_forward.hpp:57-59, fused_backward.hpp:37-39): when the targets carry
-// ignored rows, the tile kernels run on the valid rows only.  The valid count
-// is read back to size the compact problem (one stream sync, the same the
-// validation already does by default).
+// ignored rows, the valid rows are packed to the front of an N-row problem
+// (row map by a one-block scan, gather of H rows and targets, zero padding)
+// and the tile kernels skip everything past the live count, which they read
+// from device memory.  No host sync: the count never leaves the GPU, so the
+// path stays stream-ordered (and CUDA-graph capturable with validation off).
 struct Compact {
     bool on = false;
-    int64_t n_valid = 0;
     int* map = nullptr;        // [N] slot or -1
-    int* rows = nullptr;       // [n_valid] original row
+    int* rows = nullptr;       // [N] original row of each live slot
     int64_t* targets = nullptr;
-    void* hidden = nullptr;    // [n_valid, ldh] bf16
+    void* hidden = nullptr;    // [N, ldh] bf16, live rows first, zero padding
     int64_t ldh = 0;
     float* gamma = nullptr;    // backward: per-slot effective upstream / lse
     float* lse = nullptr;
-    float* dh = nullptr;       // backward: [n_valid, lddh] fp32
+    float* dh = nullptr;       // backward: [N, lddh] fp32
     int64_t lddh = 0;
 };
 
@@ -207,27 +208,20 @@ fce_status plan_compaction(fce_handle h, const fce_problem* p, bool backward, bo
                            fce_problem* pc) {
     *pc = *p;
     if (!p->has_ignore || !h->skip_ignored) return FCE_OK;
-    FCE_CUDA(cudaMemcpyAsync(h->host_err + kErrSlots, h->count, sizeof(unsigned long long),
-                             cudaMemcpyDeviceToHost, h->stream));
-    FCE_CUDA(cudaStreamSynchronize(h->stream));
-    unsigned long long cnt;
-    std::memcpy(&cnt, h->host_err + kErrSlots, sizeof(cnt));
-    const int64_t nv = static_cast<int64_t>(cnt);
-    if (nv >= p->n) return FCE_OK;
+    const int64_t n = p->n;
     c->on = true;
-    c->n_valid = nv;
     c->ldh = round_up(p->d, 8);
     c->lddh = round_up(p->d, 4);
     Scratch cs(h, &h->cws, &h->cws_size);
-    const size_t o_map = cs.take(sizeof(int) * p->n);
-    const size_t o_rows = cs.take(sizeof(int) * std::max<int64_t>(nv, 1));
-    const size_t o_t = cs.take(sizeof(int64_t) * std::max<int64_t>(nv, 1));
-    const size_t o_h = cs.take(sizeof(__nv_bfloat16) * std::max<int64_t>(nv, 1) * c->ldh);
+    const size_t o_map = cs.take(sizeof(int) * n);
+    const size_t o_rows = cs.take(sizeof(int) * n);
+    const size_t o_t = cs.take(sizeof(int64_t) * n);
+    const size_t o_h = cs.take(sizeof(__nv_bfloat16) * n * c->ldh);
     size_t o_g = 0, o_l = 0, o_dh = 0;
     if (backward) {
-        o_g = cs.take(sizeof(float) * std::max<int64_t>(nv, 1));
-        o_l = cs.take(sizeof(float) * std::max<int64_t>(nv, 1));
-        if (want_dh) o_dh = cs.take(sizeof(float) * std::max<int64_t>(nv, 1) * c->lddh);
+        o_g = cs.take(sizeof(float) * n);
+        o_l = cs.take(sizeof(float) * n);
+        if (want_dh) o_dh = cs.take(sizeof(float) * n * c->lddh);
     }
     fce_status s = cs.commit();
     if (s) return s;
@@ -240,15 +234,14 @@ fce_status plan_compaction(fce_handle h, const fce_problem* p, bool backward, bo
         c->lse = cs.ptr<float>(o_l);
         if (want_dh) c->dh = cs.ptr<float>(o_dh);
     }
-    cudaError_t e = launch_row_map(p->targets, p->n, p->ignore_index, c->map, c->rows, h->stream);
+    cudaError_t e = launch_row_map(p->targets, n, p->ignore_index, c->map, c->rows, h->stream);
     if (e == cudaSuccess)
-        e = launch_gather_rows(p->hidden, p->ldh * 2, c->hidden, c->ldh * 2, p->d * 2, c->rows, nv,
+        e = launch_gather_rows(p->hidden, p->ldh * 2, c->hidden, c->ldh * 2, p->d * 2, c->rows, n, h->count,
                                p->targets, c->targets, nullptr, nullptr, nullptr, nullptr, h->stream);
     if (e != cudaSuccess) return fail(FCE_CUDA_ERROR, "compaction kernels: %s", cudaGetErrorString(e));
-    h->launches += nv > 0 ? 3 : 1;
+    h->launches += 3;
     pc->hidden = c->hidden;
     pc->ldh = c->ldh;
-    pc->n = nv;
     pc->targets = c->targets;
     pc->has_ignore = 0;
     return FCE_OK;
@@ -343,7 +336,7 @@ FwdGeom forward_geometry(fce_handle h, const fce_problem* p, int64_t window) {
 }
 
 fce_status run_forward_tiles(fce_handle h, const fce_problem* p, const FwdGeom& g, float* pm, float* pa,
-                             float* pzt, uint8_t* pf) {
+                             float* pzt, uint8_t* pf, const unsigned long long* n_valid = nullptr) {
     TileParams tp;
     std::memset(&tp, 0, sizeof(tp));
     TensorMaps maps;
@@ -355,6 +348,7 @@ fce_status run_forward_tiles(fce_handle h, const fce_problem* p, const FwdGeom& 
         return fail(FCE_CUDA_ERROR, "cuTensorMapEncodeTiled failed for H / W");
     tp.mode = kEpiForward;
     tp.n_rows = static_cast<int>(p->n);
+    tp.n_valid = n_valid;
     tp.v_cols = static_cast<int>(p->v);
     tp.m_blocks = static_cast<int>(g.m_blocks);
     tp.v_tiles = static_cast<int>(g.v_tiles);
@@ -381,7 +375,8 @@ fce_status run_forward_tiles(fce_handle h, const fce_problem* p, const FwdGeom& 
 fce_status run_backward_persistent(fce_handle h, const fce_problem* p, const float* gamma,
                                    const float* lse, int64_t row_chunk, int64_t band, int kg,
                                    float* dhidden, int64_t lddh, float* dweight, int64_t lddw,
-                                   int accumulate_dhidden, bool dw_bf16 = false) {
+                                   int accumulate_dhidden, bool dw_bf16 = false,
+                                   const unsigned long long* n_valid = nullptr) {
     char* ws = static_cast<char*>(h->ws);
     __nv_bfloat16* g_ring = reinterpret_cast<__nv_bfloat16*>(ws + h->bwd_scratch[0]);
     unsigned* d_ctr = reinterpret_cast<unsigned*>(ws + h->bwd_scratch[1]);
@@ -419,6 +414,7 @@ fce_status run_backward_persistent(fce_handle h, const fce_problem* p, const flo
     bp.unit_mask = static_cast<int>(h->bwd_unit_mask);
     bp.epi_warps = static_cast<int>(h->bwd_epi_warps);
     bp.dw_bf16 = dw_bf16 ? 1 : 0;
+    bp.n_valid = n_valid;
     bp.trace = reinterpret_cast<unsigned long long*>(h->trace_ptr);
     bp.nc_max = row_chunk;
     bp.ldg = band;
@@ -673,9 +669,8 @@ fce_status fce_forward(fce_handle h, const fce_problem* p, int reduction, int64_
     const size_t o_b = sc.take(sizeof(double) * (ceil_div(p->n, 256) + 1));
     if ((s = sc.commit())) return s;
 
-    if (pc.n > 0 &&
-        (s = run_forward_tiles(h, &pc, geom, sc.ptr<float>(o_m), sc.ptr<float>(o_a),
-                               sc.ptr<float>(o_z), sc.ptr<uint8_t>(o_f))))
+    if ((s = run_forward_tiles(h, &pc, geom, sc.ptr<float>(o_m), sc.ptr<float>(o_a), sc.ptr<float>(o_z),
+                               sc.ptr<uint8_t>(o_f), cp.on ? h->count : nullptr)))
         return s;
     int blocks = 0;
     e = launch_merge_stats(splits, p->n, nc, sc.ptr<float>(o_m), sc.ptr<float>(o_a),
@@ -716,9 +711,8 @@ fce_status fce_forward_partial(fce_handle h, const fce_problem* p, fce_stats par
     const size_t o_z = sc.take(sizeof(float) * splits * nc);
     const size_t o_f = sc.take(splits * nc);
     if ((s = sc.commit())) return s;
-    if (pc.n > 0 &&
-        (s = run_forward_tiles(h, &pc, geom, sc.ptr<float>(o_m), sc.ptr<float>(o_a),
-                               sc.ptr<float>(o_z), sc.ptr<uint8_t>(o_f))))
+    if ((s = run_forward_tiles(h, &pc, geom, sc.ptr<float>(o_m), sc.ptr<float>(o_a), sc.ptr<float>(o_z),
+                               sc.ptr<uint8_t>(o_f), cp.on ? h->count : nullptr)))
         return s;
     e = launch_merge_stats(splits, p->n, nc, sc.ptr<float>(o_m), sc.ptr<float>(o_a),
                            sc.ptr<float>(o_z), sc.ptr<uint8_t>(o_f), p->targets, p->has_ignore,
@@ -899,25 +893,20 @@ fce_status fce_backward_ex(fce_handle h, const fce_problem* p, fce_stats stats, 
     int64_t lddh_k = lddh;
     int acc_k = accumulate_dhidden;
     if (cp.on) {
-        e = launch_gather_rows(nullptr, 0, nullptr, 0, 0, cp.rows, cp.n_valid, nullptr, nullptr, gamma,
+        e = launch_gather_rows(nullptr, 0, nullptr, 0, 0, cp.rows, p->n, h->count, nullptr, nullptr, gamma,
                                cp.gamma, lse, cp.lse, h->stream);
         if (e != cudaSuccess) return fail(FCE_CUDA_ERROR, "compaction gather: %s", cudaGetErrorString(e));
-        h->launches += cp.n_valid > 0 ? 1 : 0;
+        h->launches += 1;
         gamma = cp.gamma;
         lse = cp.lse;
         dh_k = cp.dh;
         lddh_k = cp.lddh;
         acc_k = 0;
-        if (cp.n_valid == 0 && dw_store) {
-            // nothing valid: dW is exactly zero (zero-initialised, never accumulated)
-            const size_t es = dw_direct ? sizeof(__nv_bfloat16) : sizeof(float);
-            FCE_CUDA(cudaMemset2DAsync(dw_store, lddw_k * es, 0, p->d * es, p->v, h->stream));
-        }
     }
-    if (pk->n > 0) {
+    {
         if (h->bwd_persistent) {
             s = run_backward_persistent(h, pk, gamma, lse, row_chunk, band, kg, dh_k, lddh_k, dw_store,
-                                        lddw_k, acc_k, dw_direct);
+                                        lddw_k, acc_k, dw_direct, cp.on ? h->count : nullptr);
         } else {
             s = run_backward_tiles(h, pk, gamma, lse, row_chunk, band, G, dh_k, lddh_k, dw_store, lddw_k,
                                    acc_k);

@@ -73,11 +73,15 @@ struct BUnit {
     int gcol;     // ring column of this band's G (grad, dW)
     int row_idx, gl, c0, nb;  // row chunk, group within it, its first chunk, bands
     bool empty;   // past N or V: no loads / MMA / stores, completion only
+    bool zero_dw; // dW unit of the first row chunk with no live rows: stores zeros (no MMA)
 };
 
 // Closed-form decode of the dispatch order described at the top of the file.
-__device__ __forceinline__ BUnit decode_unit(const BwdParams& p, int u) {
+// n_live: rows of the (compacted) problem that are real; the geometry is laid
+// out for p.n rows and units past n_live are empty.
+__device__ __forceinline__ BUnit decode_unit(const BwdParams& p, int u, int n_live) {
     BUnit r;
+    r.zero_dw = false;
     if (u >= p.units) {
         r.type = kUnitStop;
         r.empty = true;
@@ -119,7 +123,7 @@ __device__ __forceinline__ BUnit decode_unit(const BwdParams& p, int u) {
     }
     r.c = r.c0 + j;
     r.r0 = r.row_idx * static_cast<int>(p.nc_max);
-    r.nc = min(static_cast<int>(p.nc_max), p.n - r.r0);
+    r.nc = min(static_cast<int>(p.nc_max), n_live - r.r0);
     r.gcol = j * static_cast<int>(p.ldg);
     if (r.type == kUnitDH) {
         r.vb = r.gl * p.kg * static_cast<int>(p.ldg);
@@ -140,7 +144,14 @@ __device__ __forceinline__ BUnit decode_unit(const BwdParams& p, int u) {
             r.empty = r.m_blk * kPM >= r.vc;
         }
     }
-    if (!((p.unit_mask >> r.type) & 1)) r.empty = true;
+    if (!((p.unit_mask >> r.type) & 1)) {
+        r.empty = true;
+    } else if (r.type == kUnitDW && !r.empty && r.nc <= 0) {
+        // no live rows in this row chunk: nothing to add; the first chunk's
+        // units still owe dW its (zero) value
+        r.empty = true;
+        r.zero_dw = r.row_idx == 0;
+    }
     return r;
 }
 
@@ -242,6 +253,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(128 + 32 * kEpiWarps
     tc_fence_after();
     const uint32_t tmem_base = *tmem_slot;
     const uint32_t leader_uempty0 = mapa_shared(&uempty[0], 0);
+    // compacted problems: the live row count is produced on the device
+    const int n_live = p.n_valid ? static_cast<int>(min(static_cast<unsigned long long>(p.n), *p.n_valid)) : p.n;
 
     if (warp == kWarpSched) {
         // ------------------------------------------------ scheduler (even CTA)
@@ -263,7 +276,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(128 + 32 * kEpiWarps
                 } else {
                     u = static_cast<int>(atomicAdd(p.counters, 1u));
                 }
-                const BUnit un = decode_unit(p, u);
+                const BUnit un = decode_unit(p, u, n_live);
                 if (un.type != kUnitStop && !un.empty) {
                     if (un.type == kUnitGrad) {
                         const int g = un.row_idx * p.gpr + un.gl;
@@ -315,7 +328,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(128 + 32 * kEpiWarps
                     us = 0;
                     uphase ^= 1;
                 }
-                const BUnit un = decode_unit(p, u);
+                const BUnit un = decode_unit(p, u, n_live);
                 if (un.type == kUnitStop) break;
                 if (un.empty) continue;
                 const CUtensorMap *ma, *mb;
@@ -397,7 +410,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(128 + 32 * kEpiWarps
                     us = 0;
                     uphase ^= 1;
                 }
-                const BUnit un = decode_unit(p, u);
+                const BUnit un = decode_unit(p, u, n_live);
                 if (un.type == kUnitStop) break;
                 if (un.empty) continue;
                 const uint32_t a_mn = un.type == kUnitDW ? 1u : 0u;
@@ -473,7 +486,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(128 + 32 * kEpiWarps
                 us = 0;
                 uphase ^= 1;
             }
-            const BUnit un = decode_unit(p, u);
+            const BUnit un = decode_unit(p, u, n_live);
             if (un.type == kUnitStop) break;
 
             if (!un.empty) {
@@ -622,7 +635,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(128 + 32 * kEpiWarps
                         float v[32];
                         tmem_ld32(taddr + c * 32, v);
                         const int col0 = un.n_tile * kBN + c * 32;
-                        if (row_ok && !((p.unit_mask >> 3) & 1)) {  // debug bit 3: skip G stores
+                        // rows past the live count inside the unit store zeros (gam = 0):
+                        // dW units read them against zero H rows, so they must be finite
+                        if (!((p.unit_mask >> 3) & 1)) {  // debug bit 3: skip G stores
                             const int64_t tc = tcol - col0;
                             uint32_t packed[16];
 #pragma unroll
@@ -687,6 +702,22 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(128 + 32 * kEpiWarps
                 if (acc == 0) acc_phase ^= 1;
                 // generic-proxy stores above are read later through TMA (async proxy)
                 fence_proxy_async_global();
+            }
+
+            if (un.zero_dw) {
+                // dW rows of a launch whose row chunks hold no live row: exact zeros
+                const int lrow = un.m_blk * kPM + static_cast<int>(rank) * 128 + r;
+                if (lrow < un.vc) {
+                    const int c_per = kBN / (kEpiWarps / 4);
+                    const int c0 = un.n_tile * kBN + chalf * c_per;
+                    const int64_t vrow = static_cast<int64_t>(un.vb) + lrow;
+                    for (int c = c0; c < c0 + c_per && c < p.d; ++c) {
+                        if (p.dw_bf16)
+                            reinterpret_cast<__nv_bfloat16*>(p.dw)[vrow * p.lddw + c] = __float2bfloat16(0.f);
+                        else
+                            p.dw[vrow * p.lddw + c] = 0.f;
+                    }
+                }
             }
 
             // publish completion of this CTA's half: all 128 epilogue threads'

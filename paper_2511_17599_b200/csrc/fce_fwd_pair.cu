@@ -68,6 +68,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     const uint32_t rank = cluster_ctarank();
     const int pair = blockIdx.x >> 1;
     const int n_pairs = gridDim.x >> 1;
+    // compacted forward: row pairs past the device count of live rows are skipped
+    const int n_eff = p.n_valid ? static_cast<int>(min(static_cast<unsigned long long>(p.n_rows), *p.n_valid))
+                                : p.n_rows;
 
     if (threadIdx.x == 0) {
         for (int s = 0; s < kFS; ++s) {
@@ -99,6 +102,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         uint32_t phase = 0;
         for (int u = pair; u < p.units; u += n_pairs) {
             const FUnit un = fwd_unit(p, u);
+            if (un.m_pair * 256 >= n_eff) continue;
             const int a_row = un.m_pair * 256 + rank * 128;
             for (int t = 0; t < un.nt; ++t) {
                 const int b_row = (un.t0 + t) * kBN + rank * 128;
@@ -126,6 +130,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
             uint32_t phase = 0, acc_phase = 0;
             for (int u = pair; u < p.units; u += n_pairs) {
                 const FUnit un = fwd_unit(p, u);
+                if (un.m_pair * 256 >= n_eff) continue;
                 for (int t = 0; t < un.nt; ++t) {
                     mbar_wait(&tempty[acc], acc_phase ^ 1);
                     tc_fence_after();
@@ -159,8 +164,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         uint32_t acc_phase = 0;
         for (int u = pair; u < p.units; u += n_pairs) {
             const FUnit un = fwd_unit(p, u);
+            if (un.m_pair * 256 >= n_eff) continue;
             const int64_t row = static_cast<int64_t>(un.m_pair) * 256 + rank * 128 + r;
-            const bool row_ok = row < p.n_rows;
+            const bool row_ok = row < n_eff;
             bool skip = true;
             int64_t tcol = -1;
             if (row_ok) {

@@ -38,7 +38,9 @@ struct TileParams {
     int mode;
     int units;               // total work units
     // forward / grad (A = H [N, D] K-major, B = W rows K-major)
-    int n_rows;              // N
+    int n_rows;              // N (rows of the operand / partial arrays)
+    const unsigned long long* n_valid;  // forward: device count of live rows (compacted problems); rows
+                                        // past it are skipped on the device (NULL: all n_rows)
     int v_cols;              // valid columns of this launch (V_local for fwd, band width for grad)
     int m_blocks;            // ceil(N / kBM)
     int v_tiles;             // ceil(v_cols / kBN)
@@ -82,6 +84,7 @@ struct BwdParams {
     int epi_warps;           // 4 or 8 epilogue warps per CTA
     int tma_epi;             // 1: epilogue writes G / dH / dW through SMEM + TMA store / reduce-add
     int dw_bf16;             // 1: dW is bf16 (one row chunk, stored once from the accumulators)
+    const unsigned long long* n_valid;  // device count of live rows (compacted problems; NULL: n)
     int l2_hints;            // bit0: evict_first on dH/dW writes, bit1: evict_last on G loads,
                              // bit2: evict_last on G stores, bit3: evict_first on H loads (dW)
     int64_t nc_max, ldg, ldr, d, lddh, lddw, v_offset, ignore_index;  // ldg = band, ldr = kg * band
@@ -138,9 +141,10 @@ cudaError_t launch_round_to_bf16(const float* in, int64_t rows, int64_t cols, in
 cudaError_t launch_row_map(const int64_t* targets, int64_t n, int64_t ignore_index, int* row_map,
                            int* rows, cudaStream_t stream);
 cudaError_t launch_gather_rows(const void* src, int64_t ld_src_bytes, void* dst, int64_t ld_dst_bytes,
-                               int64_t row_bytes, const int* rows, int64_t n_rows,
-                               const int64_t* t_in, int64_t* t_out, const float* g_in, float* g_out,
-                               const float* l_in, float* l_out, cudaStream_t stream);
+                               int64_t row_bytes, const int* rows, int64_t n_slots,
+                               const unsigned long long* count, const int64_t* t_in, int64_t* t_out,
+                               const float* g_in, float* g_out, const float* l_in, float* l_out,
+                               cudaStream_t stream);
 cudaError_t launch_scatter_rows_f32(const float* src, int64_t ld_src, float* dst, int64_t ld_dst,
                                     int64_t cols, const int* row_map, int64_t n, int accumulate,
                                     cudaStream_t stream);

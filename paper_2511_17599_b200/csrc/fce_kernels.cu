@@ -102,6 +102,14 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int rank = MC ? static_cast<int>(cluster_ctarank()) : 0;
     const int u_first = MC ? static_cast<int>(blockIdx.x >> 1) : static_cast<int>(blockIdx.x);
     const int u_step = MC ? static_cast<int>(gridDim.x >> 1) : static_cast<int>(gridDim.x);
+    // compacted forward: rows past the device count are padding; every role
+    // skips the units whose (first) row block lies past it
+    const int n_eff = (EPI == kEpiForward && p.n_valid)
+                          ? static_cast<int>(min(static_cast<unsigned long long>(p.n_rows), *p.n_valid))
+                          : p.n_rows;
+    auto dead = [&](const Unit& un) {
+        return EPI == kEpiForward && (MC ? 2 * un.m_blk : un.m_blk) * kBM >= n_eff;
+    };
 
     if (threadIdx.x == 0) {
         for (int s = 0; s < kStages; ++s) {
@@ -143,6 +151,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             const uint32_t sa0 = smem_u32(sA), sb0 = smem_u32(sB);
             for (int u = u_first; u < p.units; u += u_step) {
                 Unit un = get_unit(p, u);
+                if (dead(un)) continue;
                 if (MC) un.m_blk = 2 * un.m_blk + rank;
                 const CUtensorMap* ma = un.prob ? &maps.a1 : &maps.a0;
                 const CUtensorMap* mb = un.prob ? &maps.b1 : &maps.b0;
@@ -196,6 +205,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             const uint32_t sa0 = smem_u32(sA), sb0 = smem_u32(sB);
             for (int u = u_first; u < p.units; u += u_step) {
                 const Unit un = get_unit(p, u);
+                if (dead(un)) continue;
                 int kbs = p.k_blocks;
                 uint32_t a_mn = 0, b_mn = 0;
                 if (EPI == kEpiGemm) {
@@ -246,6 +256,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         uint32_t acc_phase = 0;
         for (int u = u_first; u < p.units; u += u_step) {
             Unit un = get_unit(p, u);
+            if (dead(un)) continue;
             if (MC) un.m_blk = 2 * un.m_blk + rank;
             const int64_t row = static_cast<int64_t>(un.m_blk) * kBM + r;
 
@@ -256,7 +267,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             bool found = false;
             float lse_r = 0.f, gam = 0.f;
             if (EPI != kEpiGemm) {
-                row_ok = row < p.n_rows;
+                row_ok = row < n_eff;
                 if (row_ok) {
                     const int64_t y = p.targets[row];
                     skip = p.has_ignore && y == p.ignore_index;
@@ -633,46 +644,55 @@ cudaError_t launch_row_map(const int64_t* targets, int64_t n, int64_t ignore_ind
 }
 
 // dst[j, 0:cols) = src[rows[j], 0:cols) for 16-byte elements (cols16 per row)
+// for the live slots j < *count; slots past it (the padding of the
+// compacted problem, sized for N rows) are zero-filled
 __global__ void k_gather_rows16(const uint4* __restrict__ src, int64_t ld_src16, uint4* __restrict__ dst,
                                 int64_t ld_dst16, int64_t cols16, const int* __restrict__ rows,
-                                int64_t n_rows) {
-    const int64_t total = n_rows * cols16;
+                                int64_t n_slots, const unsigned long long* __restrict__ count) {
+    const int64_t live = static_cast<int64_t>(*count);
+    const int64_t total = n_slots * cols16;
     for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < total;
          k += (int64_t)gridDim.x * blockDim.x) {
         const int64_t j = k / cols16, c = k - j * cols16;
-        dst[j * ld_dst16 + c] = src[static_cast<int64_t>(rows[j]) * ld_src16 + c];
+        dst[j * ld_dst16 + c] = j < live ? src[static_cast<int64_t>(rows[j]) * ld_src16 + c] : make_uint4(0, 0, 0, 0);
     }
 }
 
-// per-slot row data: targets, and (backward) gamma / lse of the valid rows
-__global__ void k_gather_row_scalars(const int* __restrict__ rows, int64_t n_rows,
+// per-slot row data: targets, and (backward) gamma / lse of the live rows;
+// padding slots get target 0 and gamma = lse = 0 (they contribute nothing)
+__global__ void k_gather_row_scalars(const int* __restrict__ rows, int64_t n_slots,
+                                     const unsigned long long* __restrict__ count,
                                      const int64_t* __restrict__ t_in, int64_t* t_out,
                                      const float* __restrict__ g_in, float* g_out,
                                      const float* __restrict__ l_in, float* l_out) {
-    for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < n_rows;
+    const int64_t live = static_cast<int64_t>(*count);
+    for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < n_slots;
          j += (int64_t)gridDim.x * blockDim.x) {
-        const int64_t i = rows[j];
-        if (t_out) t_out[j] = t_in[i];
-        if (g_out) g_out[j] = g_in[i];
-        if (l_out) l_out[j] = l_in[i];
+        const bool ok = j < live;
+        const int64_t i = ok ? rows[j] : 0;
+        if (t_out) t_out[j] = ok ? t_in[i] : 0;
+        if (g_out) g_out[j] = ok ? g_in[i] : 0.f;
+        if (l_out) l_out[j] = ok ? l_in[i] : 0.f;
     }
 }
 
 cudaError_t launch_gather_rows(const void* src, int64_t ld_src_bytes, void* dst, int64_t ld_dst_bytes,
-                               int64_t row_bytes, const int* rows, int64_t n_rows,
-                               const int64_t* t_in, int64_t* t_out, const float* g_in, float* g_out,
-                               const float* l_in, float* l_out, cudaStream_t stream) {
-    if (n_rows <= 0) return cudaSuccess;
+                               int64_t row_bytes, const int* rows, int64_t n_slots,
+                               const unsigned long long* count, const int64_t* t_in, int64_t* t_out,
+                               const float* g_in, float* g_out, const float* l_in, float* l_out,
+                               cudaStream_t stream) {
+    if (n_slots <= 0) return cudaSuccess;
     if (src) {
         const int64_t cols16 = (row_bytes + 15) / 16;
-        const int64_t total = n_rows * cols16;
+        const int64_t total = n_slots * cols16;
         const int blocks = static_cast<int>(std::min<int64_t>((total + 255) / 256, 148 * 16));
         k_gather_rows16<<<blocks, 256, 0, stream>>>(static_cast<const uint4*>(src), ld_src_bytes / 16,
                                                     static_cast<uint4*>(dst), ld_dst_bytes / 16, cols16,
-                                                    rows, n_rows);
+                                                    rows, n_slots, count);
     }
-    const int blocks = static_cast<int>(std::min<int64_t>((n_rows + 255) / 256, 148 * 4));
-    k_gather_row_scalars<<<blocks, 256, 0, stream>>>(rows, n_rows, t_in, t_out, g_in, g_out, l_in, l_out);
+    const int blocks = static_cast<int>(std::min<int64_t>((n_slots + 255) / 256, 148 * 4));
+    k_gather_row_scalars<<<blocks, 256, 0, stream>>>(rows, n_slots, count, t_in, t_out, g_in, g_out, l_in,
+                                                     l_out);
     return cudaGetLastError();
 }
 

@@ -432,18 +432,20 @@ def test_ignored_row_compaction_matches_full_rows(cuda, n, d, v, frac):
     hf.close()
 
 
-def test_cuda_graph_capture_replays_the_step(cuda):
+@pytest.mark.parametrize("frac", [0.0, 0.3])
+def test_cuda_graph_capture_replays_the_step(cuda, frac):
     """With validation off the forward + backward are stream-ordered with no host
-    sync, so a training step can be captured once and replayed as a CUDA graph."""
-    H, W, Y, ign, st, rows, lred = _oracle_case(300, 136, 1500, 17, 0.0, "mean")
+    sync (ignored-row compaction keeps its live count on the device), so a
+    training step can be captured once and replayed as a CUDA graph."""
+    H, W, Y, ign, st, rows, lred = _oracle_case(300, 136, 1500, 17, frac, "mean")
     Hd, Wd, Yd = to_dev(H, W, Y)
     s = torch.cuda.Stream()
     h = fce.Handle(0, s)
     h.set_option("validate", 0)
 
     def step():
-        out = fce.fused_forward(Hd, Wd, Yd, "mean", handle=h)
-        dh, dw = fce.fused_backward_recompute(Hd, Wd, Yd, out.stats, "mean", 1.0, handle=h)
+        out = fce.fused_forward(Hd, Wd, Yd, "mean", ign, handle=h)
+        dh, dw = fce.fused_backward_recompute(Hd, Wd, Yd, out.stats, "mean", 1.0, ign, handle=h)
         return out.loss, dh, dw
 
     s.wait_stream(torch.cuda.current_stream())
