@@ -15,10 +15,14 @@
 //   kEpiGemm     plain C (+)= A . B^T with fp32 store or red.global.add; used
 //                for dW_band = G_band^T . H and dH += G_band . W_band.
 //
-// Roles (256 threads, 1 CTA / SM): warp 0 lane 0 issues TMA into a 4-stage
-// smem ring, warp 1 lane 0 issues tcgen05.mma (M=128, N=256, K=16) into one
-// of two TMEM accumulators (2 x 256 fp32 columns), warp 2 owns the TMEM
-// allocation, warps 4-7 drain TMEM with tcgen05.ld (thread = row).
+// Roles (256 threads, 1 CTA / SM): warp 0 (converged, one elect.sync lane
+// per instruction) issues TMA into a 4-stage smem ring, warp 1 likewise issues
+// tcgen05.mma (M=128, N=256, K=16) into one of two TMEM accumulators
+// (2 x 256 fp32 columns), warp 2 owns the TMEM allocation, warps 4-7 drain
+// TMEM with tcgen05.ld (thread = row).  Template flag MC: the forward on
+// 2-CTA clusters with the W tile multicast to both CTAs (option fwd_mc).
+// Compacted problems (ignored rows packed away) pass the device-resident live
+// row count in TileParams::n_valid; the forward skips row blocks past it.
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
