@@ -78,6 +78,19 @@ if "cublas" in work:
           flush=True)
     hg.close()
     del A, B, C, Sx, Cf
+if "copy" in work:
+    # energy per byte: DRAM streaming (2 GiB copy) vs L2-resident (16 MiB copy)
+    for nbytes, tag in ((2 << 30, "DRAM"), (16 << 20, "L2")):
+        src = torch.empty(nbytes // 2, dtype=torch.bfloat16, device="cuda").uniform_()
+        dst = torch.empty_like(src)
+        reps = max(1, (256 << 20) // nbytes) if tag == "L2" else 1
+
+        def cp():
+            for _ in range(reps):
+                dst.copy_(src)
+        r = measure(cp, 2.0 * nbytes * reps)  # "flops" slot = bytes moved (read + write)
+        print(f"copy {tag:4s} {nbytes >> 20} MiB x{reps}: {r}  (TF/s = TB/s, J/PFLOP = J/PB)", flush=True)
+        del src, dst
 fl = 2.0 * n * d * v
 for s in a.sets:
     h = fce.Handle(0)
