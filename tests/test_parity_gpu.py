@@ -704,3 +704,26 @@ def test_full_size_configs(cuda, name, n, d, v, frac):
     # linearity: upstream 2 doubles both gradients exactly
     dh2, dw2 = fce.fused_backward_recompute(Hd, Wd, Yd, out.stats, "sum", 2.0, ign)
     assert torch.equal(dh2, 2 * dh) and torch.equal(dw2, 2 * dw)
+
+
+@pytest.mark.slow
+def test_rows_times_width_beyond_int32(cuda):
+    """N x D > 2^31 elements (262221 x 8192): 64-bit addressing in every kernel;
+    a row slice against the oracle, ignored rows, dW column sums."""
+    n, d, v = 262144 + 77, 8192, 4096 + 13
+    Hd, Wd, Yd = fce.generate_instance(n, d, v, 5, -100, 0.1)
+    out = fce.fused_forward(Hd, Wd, Yd, "sum", -100)
+    dh, dw = fce.fused_backward_recompute(Hd, Wd, Yd, out.stats, "sum", 1.0, -100)
+    idx = [0, 1, n // 2, n - 2, n - 1]
+    Hs = Hd[idx].float().cpu().numpy()
+    Ys = Yd[idx].cpu().numpy()
+    Wn = Wd.float().cpu().numpy()
+    st, rows, _ = ob.forward(Hs, Wn, Ys, "none", -100)
+    got = out.loss_rows[idx].cpu().numpy()
+    assert np.max(np.abs(got - rows) / np.maximum(1.0, np.abs(rows))) < LOSS_RTOL
+    dH_ref, _ = ob.backward(Hs, Wn, Ys, st, "sum", 1.0, -100, want_dw=False)
+    assert relmax(dh[idx].cpu().numpy(), dH_ref) < GRAD_RTOL
+    ignored = Yd == -100
+    assert torch.count_nonzero(dh[ignored]).item() == 0
+    col = dw.double().sum(0)
+    assert col.abs().max().item() < 1e-3 * dw.abs().max().item() * math.sqrt(v)
