@@ -727,3 +727,31 @@ def test_rows_times_width_beyond_int32(cuda):
     assert torch.count_nonzero(dh[ignored]).item() == 0
     col = dw.double().sum(0)
     assert col.abs().max().item() < 1e-3 * dw.abs().max().item() * math.sqrt(v)
+
+
+def test_repeated_calls_keep_memory_flat(cuda):
+    """200 fwd+bwd calls (with timing events and compaction on): the library
+    workspace and torch's allocations stay flat after the first call."""
+    H, W, Y, ign, st, rows, lred = _oracle_case(500, 128, 4000, 61, 0.3, "mean")
+    Hd, Wd, Yd = to_dev(H, W, Y)
+    h = fce.Handle(0)
+    h.set_option("timing", 1)
+
+    def step():
+        out = fce.fused_forward(Hd, Wd, Yd, "mean", ign, handle=h)
+        dh, dw = fce.fused_backward_recompute(Hd, Wd, Yd, out.stats, "mean", 1.0, ign, handle=h)
+        return out.loss
+
+    step()
+    torch.cuda.synchronize()
+    ws0 = h.workspace_bytes()
+    mem0 = torch.cuda.memory_allocated()
+    for _ in range(200):
+        loss = step()
+    torch.cuda.synchronize()
+    assert h.workspace_bytes() == ws0
+    assert torch.cuda.memory_allocated() <= mem0 + 4096
+    ms, launches, flops = h.kernel_stats(0)
+    assert launches >= 200 and ms > 0
+    assert abs(loss.item() - lred) <= LOSS_RTOL * abs(lred)
+    h.close()
