@@ -106,6 +106,25 @@ def fused_linear_cross_entropy(hidden: torch.Tensor, weight: torch.Tensor, targe
     return loss
 
 
+class FusedLinearCrossEntropyLoss(torch.nn.Module):
+    """Drop-in for ``F.cross_entropy(hidden @ lm_head.weight.T, targets)`` in a
+    training step: ``loss = FusedLinearCrossEntropyLoss()(hidden, lm_head.weight, targets)``.
+    hidden may carry leading batch dims ([B, T, D] is flattened to [B*T, D])."""
+
+    def __init__(self, reduction: str = "mean", ignore_index: int = -100):
+        super().__init__()
+        if reduction not in fce.REDUCTIONS:
+            raise fce.UnsupportedReduction(reduction)
+        self.reduction = reduction
+        self.ignore_index = ignore_index
+
+    def forward(self, hidden: torch.Tensor, weight: torch.Tensor, targets: torch.Tensor) -> torch.Tensor:
+        lead = hidden.shape[:-1]
+        loss = fused_linear_cross_entropy(hidden.reshape(-1, hidden.shape[-1]), weight, targets.reshape(-1),
+                                          self.reduction, self.ignore_index)
+        return loss.reshape(lead) if self.reduction == "none" else loss
+
+
 def canonical_linear_cross_entropy(hidden, weight, targets, reduction="mean", ignore_index=None):
     """The two-stage baseline (lm_head GEMM + cross-entropy) the paper compares
     against (Table 2 "canonical"); materialises the N x V logits."""

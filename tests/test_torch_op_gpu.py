@@ -76,3 +76,24 @@ def test_torch_compile_traces_the_op(cuda):
         outs.append((loss.detach(), h.grad, w.grad))
     for a, b in zip(*outs):
         assert torch.equal(a, b)
+
+
+def test_loss_module_with_batch_dims(cuda):
+    """FusedLinearCrossEntropyLoss on [B, T, D] hidden states matches the
+    canonical torch loss (ignore_index -100) and trains an lm_head."""
+    from paper_2511_17599_b200.torch_op import FusedLinearCrossEntropyLoss
+    torch.manual_seed(0)
+    B, T, D, V = 3, 70, 96, 1500
+    hidden = (torch.randn(B, T, D, device="cuda") / D ** 0.5).to(torch.bfloat16).requires_grad_(True)
+    head = torch.nn.Linear(D, V, bias=False, device="cuda", dtype=torch.bfloat16)
+    targets = torch.randint(0, V, (B, T), device="cuda")
+    targets[:, :10] = -100
+    loss = FusedLinearCrossEntropyLoss()(hidden, head.weight, targets)
+    loss.backward()
+    ref = canonical_linear_cross_entropy(hidden.detach().float().reshape(-1, D), head.weight.detach().float(),
+                                         targets.reshape(-1), "mean", -100)
+    assert abs(loss.item() - ref.item()) <= 1e-3 * abs(ref.item())
+    assert head.weight.grad is not None and head.weight.grad.dtype == torch.bfloat16
+    assert hidden.grad.shape == (B, T, D)
+    per_tok = FusedLinearCrossEntropyLoss("none")(hidden.detach(), head.weight.detach(), targets)
+    assert per_tok.shape == (B, T) and torch.all(per_tok[:, :10] == 0)
