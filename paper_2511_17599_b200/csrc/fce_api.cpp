@@ -61,7 +61,7 @@ struct fce_handle_s {
     int64_t bwd_unit_mask = 7;
     int64_t trace_ptr = 0;
     int64_t bwd_epi_warps = 8;
-    int64_t bwd_tma_epi = 1;
+    int64_t bwd_tma_epi = 3;
     int64_t dh_group = 1;     // bands per dH group in the persistent backward
     int64_t skip_ignored = 1; // compact away ignored rows before the tile kernels
     // compaction buffers (grow-only, separate from ws so both can be live)
@@ -463,9 +463,9 @@ fce_status run_backward_persistent(fce_handle h, const fce_problem* p, const flo
         if (ok && dweight)
             ok = dw_bf16 ? encode_map_2d(&maps.dw_st, dweight, p->d, p->v, lddw * 2, 64, 128)
                          : encode_map_2d(&maps.dw_st, dweight, p->d, p->v, lddw * 4, 32, 128, true);
-        bp.tma_epi = ok ? 1 : 0;
+        bp.tma_epi = ok ? static_cast<int>(h->bwd_tma_epi & 3) : 0;
     }
-    if (dw_bf16 && !bp.tma_epi)
+    if (dw_bf16 && !(bp.tma_epi & 2))
         return fail(FCE_CUDA_ERROR, "bf16 dW needs the TMA epilogue (16-byte aligned rows)");
     cudaEvent_t e0 = nullptr, e1 = nullptr;
     if (h->timing) {
@@ -580,7 +580,8 @@ fce_status fce_set_option(fce_handle h, const char* key, int64_t value) {
     } else if (!std::strcmp(key, "validate")) {
         h->validate = value ? 1 : 0;
     } else if (!std::strcmp(key, "bwd_tma_epi")) {
-        h->bwd_tma_epi = value ? 1 : 0;
+        // 0: per-thread stores, 1: G via TMA, 2: dH / dW via TMA, 3: both
+        h->bwd_tma_epi = value > 3 ? 3 : value;
     } else if (!std::strcmp(key, "bwd_epi_warps")) {
         if (value != 4 && value != 8) return fail(FCE_INVALID_ARGUMENT, "bwd_epi_warps must be 4 or 8");
         h->bwd_epi_warps = value;
@@ -858,7 +859,7 @@ fce_status fce_backward_ex(fce_handle h, const fce_problem* p, fce_stats stats, 
     // end); dW goes out as bf16 straight from the accumulators when it is written
     // once (persistent backward, one row chunk, TMA epilogue), else via fp32
     const int64_t ld32 = round_up(p->d, 4);
-    const bool dw_direct = dw_bf16 && h->bwd_persistent && n_rc == 1 && h->bwd_tma_epi && lddw % 8 == 0 &&
+    const bool dw_direct = dw_bf16 && h->bwd_persistent && n_rc == 1 && (h->bwd_tma_epi & 2) && lddw % 8 == 0 &&
                            aligned16(dweight_out);
     const size_t o_dhf = dh_bf16 ? sc.take(sizeof(float) * p->n * ld32) : 0;
     const size_t o_dwf = (dw_bf16 && !dw_direct) ? sc.take(sizeof(float) * p->v * ld32) : 0;

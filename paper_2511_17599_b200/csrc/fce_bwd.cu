@@ -495,7 +495,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(128 + 32 * kEpiWarps
                 const uint32_t taddr = tmem_base + (static_cast<uint32_t>(q * 32) << 16) +
                                        static_cast<uint32_t>(acc * kBN);
                 const int lrow = un.m_blk * kPM + static_cast<int>(rank) * 128 + r;
-                if (p.tma_epi) {
+                // tma_epi bit 0: G through SMEM + TMA store; bit 1: dH / dW through
+                // SMEM + TMA store / reduce-add (otherwise per-thread vector stores)
+                if (un.type == kUnitGrad ? (p.tma_epi & 1) : (p.tma_epi & 2)) {
                     // Each column group (4 warps, one TMEM lane quarter each) stages a
                     // 128-row x 128-byte slice in swizzled SMEM and one thread hands it
                     // to the TMA engine: full-line stores / reduce-adds instead of 32

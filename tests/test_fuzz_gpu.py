@@ -19,6 +19,8 @@ OPTION_SETS = [
     {"row_chunk": 512, "band_cols": 256, "dh_group": 3},
     {"bwd_epi_warps": 4},
     {"bwd_tma_epi": 0},
+    {"bwd_tma_epi": 1},
+    {"bwd_tma_epi": 2},
     {"splits": 3},
 ]
 
