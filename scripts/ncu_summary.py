@@ -15,7 +15,7 @@ shutil.copy(launches, os.path.join(prof, f"{tag}_launches.csv"))
 
 def short(name):
     if "fce_bwd_persistent" in name: return "fce_bwd_persistent_sm100"
-    if "fce_tile_kernel<0>" in name: return "fce_fwd_sm100"
+    if "fce_tile_kernel<0>" in name or "fce_tile_kernel<0, " in name: return "fce_fwd_sm100"
     if "fce_tile_kernel<1>" in name: return "fce_bwd_grad_sm100"
     if "fce_tile_kernel<2>" in name: return "fce_bwd_gemm_sm100"
     return name.split("(")[0].replace("void ", "")
