@@ -460,7 +460,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(128 + 32 * kEpiWarps
                 umma_commit_pair_w(&tfull[acc], 0x3);
                 if (p.trace && lane == 0) {
                     p.trace[8 * u + 1] = global_ns();
-                    p.trace[8 * u + 6] = wait_cyc;
                     p.trace[8 * u + 7] = clock64() - cyc0;
                 }
                 acc ^= 1;
@@ -491,6 +490,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(128 + 32 * kEpiWarps
 
             if (!un.empty) {
                 mbar_wait(&tfull[acc], acc_phase);
+                // trace slot 6: when the unit's last MMA completed (accumulator full)
+                if (p.trace && rank == 0 && threadIdx.x == 0) p.trace[8 * u + 6] = global_ns();
                 tc_fence_after();
                 const uint32_t taddr = tmem_base + (static_cast<uint32_t>(q * 32) << 16) +
                                        static_cast<uint32_t>(acc * kBN);
