@@ -4,7 +4,7 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import paper_2511_17599_b200 as fce
 n, d, v = 16384, 4096, 128256
 opts = dict(kv.split("=") for kv in sys.argv[1:])
-rc, bc = int(opts.get("row_chunk", 16384)), int(opts.get("band_cols", 2048))
+rc, bc = int(opts.get("row_chunk", 16384)), int(opts.get("band_cols", 3072))
 H, W, Y = fce.generate_instance(n, d, v, 42)
 h = fce.default_handle(0)
 for k, val in opts.items(): h.set_option(k, int(val))
@@ -36,7 +36,6 @@ for k, name in enumerate(["grad", "dH", "dW"]):
     span = (t[s, 1] - t[s, 0]) / 1e3
     acc_wait = (t[s, 4] - t[s, 0]) / 1e3
     first = (t[s, 5] - t[s, 4]) / 1e3
-    steady = t[s, 6] / clk
     epi = (t[s, 2] - t[s, 1]) / 1e3
     print(f"{name:4s}: n={s.sum():6d} span {span.mean():6.1f} us = acc-free wait {acc_wait.mean():5.1f} + first-stage {first.mean():5.1f} "
           f"+ rest {span.mean()-acc_wait.mean()-first.mean():6.1f} (of which stage waits ~{steady.mean():5.1f});"
