@@ -27,9 +27,10 @@ $(DROPIN_TEST): tests/cpp/test_dropin.cpp $(wildcard include/fusedce/*.hpp inclu
 	    -Wl,-rpath,'$$ORIGIN/../../$(PKG)' -Wl,-rpath,'$$ORIGIN/../../oracle' -Wl,-rpath,/usr/local/cuda/lib64
 
 $(LIB): $(CSRC)/fce_kernels.cu $(CSRC)/fce_bwd.cu $(CSRC)/fce_pair.cu $(CSRC)/fce_fwd_pair.cu $(CSRC)/fce_api.cpp $(CSRC)/fce_vp.cpp $(CSRC)/fce_internal.h \
+        $(CSRC)/fce_comm.cpp $(CSRC)/fce_comm.cu $(CSRC)/fce_comm.h include/fce/fce_vp.h \
         $(CSRC)/sm100_ptx.cuh include/fce/fce.h
 	$(NVCC) $(NVFLAGS) -shared -cudart static -o $@ $(CSRC)/fce_kernels.cu $(CSRC)/fce_bwd.cu $(CSRC)/fce_pair.cu $(CSRC)/fce_fwd_pair.cu $(CSRC)/fce_api.cpp \
-	    $(CSRC)/fce_vp.cpp -ldl -lpthread -lrt
+	    $(CSRC)/fce_vp.cpp $(CSRC)/fce_comm.cpp $(CSRC)/fce_comm.cu -ldl -lpthread -lrt
 
 $(ORACLE): oracle/fce_oracle.c oracle/fce_oracle.h
 	$(CC) -O2 -std=c11 -fPIC -shared -fopenmp -ffp-contract=off -o $@ oracle/fce_oracle.c -lm

@@ -87,6 +87,8 @@ typedef struct fce_stats {
 /* ---------------------------------------------------------------- handle */
 fce_status fce_create(fce_handle* out, int device, void* stream /* cudaStream_t, may be NULL */);
 fce_status fce_destroy(fce_handle h);
+/* Retarget the handle; the new stream is ordered after the work already queued
+ * on the old one (the handle's workspaces are shared between them). */
 fce_status fce_set_stream(fce_handle h, void* stream);
 const char* fce_last_error(void);
 const char* fce_status_string(fce_status s);
@@ -159,6 +161,16 @@ fce_status fce_backward_ex(fce_handle h, const fce_problem* p, fce_stats stats, 
                            float upstream_scalar, const float* upstream_rows, void* dhidden,
                            int64_t lddh, int dh_dtype, void* dweight, int64_t lddw, int dw_dtype,
                            int accumulate_dhidden);
+
+/* fce_backward_ex with the MEAN / SUM upstream scalar read from device memory
+ * (one float, e.g. a framework's loss gradient tensor) instead of passed by
+ * value: no host read of the gradient, so with option "validate" = 0 an
+ * autograd backward is stream-ordered end to end and CUDA-graph capturable.
+ * reduction NONE takes upstream_rows as fce_backward_ex. */
+fce_status fce_backward_dev(fce_handle h, const fce_problem* p, fce_stats stats, int reduction,
+                            const float* upstream_scalar_dev, const float* upstream_rows, void* dhidden,
+                            int64_t lddh, int dh_dtype, void* dweight, int64_t lddw, int dw_dtype,
+                            int accumulate_dhidden);
 
 /* The tile kernel's generic contraction (the dW / dH building block), exposed
  * for kernel-level tests and benchmarks: C[M, N] (+)= A . B^T in fp32 with bf16

@@ -1,12 +1,24 @@
 /*
- * fce_vp.h — vocabulary-parallel (tensor-parallel over the vocab) C-ABI.
+ * fce_vp.h — multi-rank C-ABI: vocabulary-parallel (tensor-parallel over the
+ * vocab), sequence-parallel gather / scatter and the data-parallel step.
  *
  * Replaces the single-process rank simulation of the reference
- * (proj/include/fusedce/parallel_sim.hpp:158-290: tp_rank_partial,
- * tp_forward, tp_backward) with one process per GPU and NCCL over
- * NVLink / NVSwitch.  Each rank passes its own contiguous ceil-first W shard
- * (ShardLayout::tensor_parallel, parallel_sim.hpp:55-57, exec.hpp:25-41) in
- * an fce_problem with v_offset / v_total set; H and targets are replicated.
+ * (proj/include/fusedce/parallel_sim.hpp:158-378: tp_rank_partial,
+ * tp_forward, tp_backward, sp_to_tp_gather, dp_step) with real ranks.  Each
+ * rank passes its own contiguous ceil-first W shard (ShardLayout::
+ * tensor_parallel, parallel_sim.hpp:55-57, exec.hpp:25-41) in an fce_problem
+ * with v_offset / v_total set; H and targets are replicated.
+ *
+ * A communicator (fce_comm) has one of two transports:
+ *   NCCL  (fce_comm_init)        one process per GPU, NCCL over NVLink /
+ *                                NVSwitch — the production layout;
+ *   local (fce_comm_init_local)  k ranks inside ONE process, each driven by
+ *                                its own host thread, on any devices (several
+ *                                may share one GPU); collectives are the
+ *                                library's own peer-memory kernels.
+ * Every collective entry point must be called by all ranks of the
+ * communicator (for the local transport: concurrently, one thread per rank).
+ * All device work is stream-ordered on the handle's stream.
  */
 #ifndef FCE_FCE_VP_H_
 #define FCE_FCE_VP_H_
@@ -18,27 +30,73 @@ extern "C" {
 #endif
 
 typedef struct fce_comm_s* fce_comm;
+typedef struct fce_comm_group_s* fce_comm_group;
 
 #define FCE_COMM_ID_BYTES 128
 
-/* Rank 0 creates the id and ships it to the others (e.g. torch.distributed
- * broadcast); every rank then calls fce_comm_init. */
+enum { FCE_TRANSPORT_NCCL = 1, FCE_TRANSPORT_LOCAL = 2 };
+
+/* NCCL transport: rank 0 creates the id and ships it to the others (e.g. a
+ * torch.distributed broadcast); every rank then calls fce_comm_init. */
 fce_status fce_comm_unique_id(uint8_t* out, size_t len);
 fce_status fce_comm_init(fce_comm* out, int device, int nranks, int rank, const uint8_t* id,
                          size_t len);
+/* Local transport: one group object shared by the k ranks of this process. */
+fce_status fce_comm_group_create(fce_comm_group* out, int nranks);
+fce_status fce_comm_group_destroy(fce_comm_group g); /* the group lives on until its last comm is destroyed */
+fce_status fce_comm_init_local(fce_comm* out, fce_comm_group g, int device, int rank);
 fce_status fce_comm_destroy(fce_comm c);
+fce_status fce_comm_query(fce_comm c, int* nranks, int* rank, int* transport);
 const char* fce_vp_last_error(void);
+/* Bytes of device scratch the communicator holds (gather / pack buffers). */
+fce_status fce_comm_scratch_bytes(fce_comm c, size_t* bytes);
 
-/* tp_forward (parallel_sim.hpp:186-236): all-gather of the per-row
- * (m, a, z_target, found) partials + rank-ordered merge; every rank ends with
- * the same merged stats, lse and loss. */
+/* Raw collectives on the handle's stream (fp32 sums are added in rank order
+ * on the local transport). */
+fce_status fce_comm_all_gather(fce_handle h, fce_comm c, const void* send, void* recv, size_t bytes_per_rank);
+fce_status fce_comm_all_reduce_f32(fce_handle h, fce_comm c, const float* send, float* recv, size_t count);
+fce_status fce_comm_reduce_scatter_f32(fce_handle h, fce_comm c, const float* send, float* recv,
+                                       size_t recv_count);
+
+/* tp_forward (parallel_sim.hpp:186-236): this rank's partial stats over its
+ * shard, one all-gather of the packed (m, a, z_target, found) block — 13 B per
+ * row per rank — and a rank-ordered merge on every rank, so every rank ends
+ * with the same merged stats, lse and loss. */
 fce_status fce_vp_forward(fce_handle h, fce_comm c, const fce_problem* p, int reduction,
                           fce_stats merged, float* lse, float* loss_rows, float* loss_reduced);
 
-/* tp_backward (parallel_sim.hpp:246-290): local dW shard, all-reduced dH. */
+/* tp_backward (parallel_sim.hpp:246-290): local dW shard, dH summed over
+ * ranks (every rank ends with the full dH).  Any lddh >= d (a strided dH is
+ * reduced through a packed buffer). */
 fce_status fce_vp_backward(fce_handle h, fce_comm c, const fce_problem* p, fce_stats merged,
                            int reduction, float upstream_scalar, const float* upstream_rows,
                            float* dhidden, int64_t lddh, float* dweight_shard, int64_t lddw);
+
+/* sp_to_tp_gather (parallel_sim.hpp:294-314): rank r holds position shard r
+ * of H (bf16 [shard_rows, ld_shard]; shards are consecutive in rank order,
+ * e.g. the ceil-first partition_ranges(n_total, nranks)); every rank receives
+ * the full H (bf16 [n_total, ld_full]) in position order.  Shards may be ragged; the
+ * ranks exchange their (rows, d) first (one host sync): rows that do not add
+ * up to n_total -> FCE_DIMENSION_MISMATCH, disagreeing widths ->
+ * FCE_INVALID_LAYOUT (sp_to_tp_gather's "hidden shards disagree on width"). */
+fce_status fce_sp_gather(fce_handle h, fce_comm c, const void* shard, int64_t shard_rows, int64_t ld_shard,
+                         int64_t d, int64_t n_total, void* full, int64_t ld_full);
+
+/* The backward's inverse of fce_sp_gather: every rank holds a full-length dH
+ * partial (fp32 [n_total, lddh], e.g. its vocab shard's contribution); rank r
+ * receives the sum over ranks of rows of its position shard (a reduce-scatter
+ * in place of fce_vp_backward's all-reduce when the caller is sequence
+ * parallel). */
+fce_status fce_sp_scatter(fce_handle h, fce_comm c, const float* dh_partial, int64_t n_total, int64_t lddh,
+                          int64_t d, float* dh_shard, int64_t shard_rows, int64_t ld_shard);
+
+/* dp_step (parallel_sim.hpp:334-378): every rank runs the fused forward and
+ * backward on its micro-batch (p), then loss and dW are averaged over the
+ * ranks (all-reduce / nranks); dH stays rank-local (may be NULL).  Micro-
+ * batches must have equal sizes (FCE_INVALID_LAYOUT), and reduction must be
+ * mean or sum (FCE_UNSUPPORTED_REDUCTION).  loss: one device float. */
+fce_status fce_dp_step(fce_handle h, fce_comm c, const fce_problem* p, int reduction, float* loss,
+                       float* dhidden, int64_t lddh, float* dweight, int64_t lddw);
 
 #ifdef __cplusplus
 }

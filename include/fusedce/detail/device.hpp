@@ -7,6 +7,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <algorithm>
 #include <cstring>
 #include <map>
 #include <string>
@@ -91,22 +92,31 @@ void require_float() {
 
 inline std::int64_t padded_ld(std::size_t cols) { return static_cast<std::int64_t>((cols + 7) / 8 * 8); }
 
-// float rows on the bf16 grid -> device bf16 [rows, ld] (exact conversion)
+// float rows on the bf16 grid -> device bf16 [rows, ld] (exact conversion).
+// The rows go up as fp32 in chunks of <= 64 MB and are checked and converted
+// on the device (fce_f32_to_bf16: off-grid values -> InvalidLayout), so the
+// host never walks the V x D weights element by element.
 inline DeviceBuffer upload_bf16(const float* src, std::size_t rows, std::size_t cols, std::int64_t ld,
                                 const char* name) {
-    std::vector<std::uint16_t> staged(rows * static_cast<std::size_t>(ld), 0);
-    for (std::size_t r = 0; r < rows; ++r) {
-        const float* s = src + r * cols;
-        std::uint16_t* d = staged.data() + r * static_cast<std::size_t>(ld);
-        for (std::size_t c = 0; c < cols; ++c) {
-            if (!is_bf16_value(s[c]))
-                throw InvalidLayout(std::string(name) + " value at (" + std::to_string(r) + ", " + std::to_string(c) +
-                                    ") is not on the bf16 grid (round_to_bf16 first)");
-            d[c] = bf16_bits(s[c]);
-        }
+    int dev = 0;
+    cuda_check(cudaGetDevice(&dev), "cudaGetDevice");
+    fce_handle h = handle_for(dev);
+    DeviceBuffer buf(rows * static_cast<std::size_t>(ld) * sizeof(std::uint16_t));
+    if (!rows || !cols) return buf;
+    const std::size_t chunk = std::max<std::size_t>(1, (std::size_t(16) << 20) / cols);
+    DeviceBuffer f32(std::min(chunk, rows) * cols * sizeof(float));
+    cuda_check(cudaMemset(buf.get(), 0, buf.bytes()), "cudaMemset");
+    for (std::size_t r0 = 0; r0 < rows; r0 += chunk) {
+        const std::size_t nr = std::min(chunk, rows - r0);
+        f32.upload(src + r0 * cols, nr * cols * sizeof(float));
+        const fce_status s = fce_f32_to_bf16(h, f32.get<float>(), static_cast<std::int64_t>(nr),
+                                             static_cast<std::int64_t>(cols), static_cast<std::int64_t>(cols),
+                                             buf.get<std::uint16_t>() + r0 * static_cast<std::size_t>(ld), ld);
+        if (s == FCE_INVALID_LAYOUT)
+            throw InvalidLayout(std::string(name) + " has a value in rows [" + std::to_string(r0) + ", " +
+                                std::to_string(r0 + nr) + ") that is not on the bf16 grid (round_to_bf16 first)");
+        throw_status(s, "upload");
     }
-    DeviceBuffer buf(staged.size() * sizeof(std::uint16_t));
-    buf.upload(staged.data(), buf.bytes());
     return buf;
 }
 

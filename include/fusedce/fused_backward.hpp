@@ -44,7 +44,9 @@ Gradients<T> backward_device(const MatrixView<T>& hidden, const MatrixView<T>& w
         std::vector<float> u(up_rows->begin(), up_rows->end());
         up.upload(u.data(), n * 4);
     }
-    ScopedCharge charge(ledger, staged_bytes(dp) + 3 * n * 4 + n + up.bytes() + dh.bytes() + dw.bytes());
+    // the reference's accounting (fused_backward.hpp:128, 135): gamma and the
+    // two gradient buffers; the device path has no private dW partials
+    ScopedCharge charge(ledger, n * sizeof(T) + (n + v) * d * sizeof(T));
     fce_stats st{m.get<float>(), a.get<float>(), z.get<float>(), f.get<std::uint8_t>()};
     throw_status(fce_backward(handle_for(policy.device), &dp.p, st, to_fce(reduction), static_cast<float>(up_scalar),
                               up_rows ? up.get<float>() : nullptr, dh.get<float>(), static_cast<std::int64_t>(d),

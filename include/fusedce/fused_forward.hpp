@@ -87,7 +87,11 @@ FusedOutput<T> forward_device(const MatrixView<T>& hidden, const MatrixView<T>& 
     DeviceProblem dp = upload_problem(hidden, weights, targets);
     const std::size_t n = dims.n;
     DeviceBuffer m(n * 4), a(n * 4), z(n * 4), f(n), rows(n * 4), red(4);
-    ScopedCharge charge(ledger, staged_bytes(dp) + 4 * n * 4 + n + 4);
+    // the reference's accounting of forward_core (fused_forward.hpp:103-105):
+    // merged + window stats and the per-row losses, independent of V.  The
+    // device copies of the inputs are staging, not auxiliary memory (the
+    // library's own workspace is reported by fce_workspace_bytes).
+    ScopedCharge charge(ledger, 2 * n * sizeof(SoftmaxStats<T>) + n * sizeof(T));
     fce_handle h = handle_for(policy.device);
     fce_stats st{m.get<float>(), a.get<float>(), z.get<float>(), f.get<std::uint8_t>()};
     throw_status(fce_forward(h, &dp.p, to_fce(reduction), static_cast<std::int64_t>(window), st, nullptr,
@@ -141,9 +145,11 @@ SoftmaxStats<T> stream_stats(std::span<const T> h, const MatrixView<T>& weights,
         throw DimensionMismatch("vocab range [" + std::to_string(lo) + ", " + std::to_string(hi) +
                                 ") not contained in [0, " + std::to_string(weights.rows) + ")");
     if (lo == hi) return SoftmaxStats<T>{};
-    // target outside the range: use a sentinel the kernel never matches
+    // target outside [lo, hi) (or none): a sentinel the kernel never matches —
+    // the reference never validates it, the result just has found = false
     const std::int64_t y = target.value_or(-1);
-    TargetVector tv(std::vector<std::int64_t>{y >= 0 ? y : static_cast<std::int64_t>(hi)});
+    const bool in_range = y >= static_cast<std::int64_t>(lo) && y < static_cast<std::int64_t>(hi);
+    TargetVector tv(std::vector<std::int64_t>{in_range ? y : static_cast<std::int64_t>(hi)});
     MatrixView<T> row(h.data(), 1, h.size());
     detail::DeviceProblem dp = detail::upload_problem(row, weights.rows_slice(lo, hi), tv, lo, 0);
     dp.p.v_total = static_cast<std::int64_t>(std::max<std::size_t>(hi + 1, weights.rows + 1));

@@ -79,10 +79,13 @@ class FceStats(ctypes.Structure):
 EXPORTED_SYMBOLS = [
     "fce_create", "fce_destroy", "fce_set_stream", "fce_last_error", "fce_status_string",
     "fce_set_option", "fce_workspace_bytes", "fce_launch_count", "fce_kernel_stats", "fce_forward",
-    "fce_forward_partial", "fce_merge_partials", "fce_backward", "fce_backward_ex", "fce_gemm_bf16", "fce_scale",
+    "fce_forward_partial", "fce_merge_partials", "fce_backward", "fce_backward_ex", "fce_backward_dev",
+    "fce_gemm_bf16", "fce_scale",
     "fce_generate_instance", "fce_f32_to_bf16",
-    "fce_comm_unique_id", "fce_comm_init", "fce_comm_destroy", "fce_vp_last_error",
-    "fce_vp_forward", "fce_vp_backward",
+    "fce_comm_unique_id", "fce_comm_init", "fce_comm_group_create", "fce_comm_group_destroy",
+    "fce_comm_init_local", "fce_comm_destroy", "fce_comm_query", "fce_vp_last_error", "fce_comm_scratch_bytes",
+    "fce_comm_all_gather", "fce_comm_all_reduce_f32", "fce_comm_reduce_scatter_f32",
+    "fce_vp_forward", "fce_vp_backward", "fce_sp_gather", "fce_sp_scatter", "fce_dp_step",
 ]
 
 _lib = None
@@ -115,13 +118,26 @@ def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
         "fce_backward": (I32, [P, ctypes.POINTER(FceProblem), FceStats, I32, F, P, P, I64, P, I64, I32]),
         "fce_backward_ex": (I32, [P, ctypes.POINTER(FceProblem), FceStats, I32, F, P, P, I64, I32, P, I64, I32,
                                   I32]),
+        "fce_backward_dev": (I32, [P, ctypes.POINTER(FceProblem), FceStats, I32, P, P, P, I64, I32, P, I64, I32,
+                                   I32]),
         "fce_scale": (I32, [P, P, I64, F]),
         "fce_gemm_bf16": (I32, [P, P, I64, I32, P, I64, I32, I64, I64, I64, P, I64, I32]),
         "fce_generate_instance": (I32, [P, I64, I64, I64, ctypes.c_uint64, P, I64, P, I64, P, I64, D, P, P]),
         "fce_f32_to_bf16": (I32, [P, P, I64, I64, I64, P, I64]),
         "fce_comm_unique_id": (I32, [P, ctypes.c_size_t]),
         "fce_comm_init": (I32, [ctypes.POINTER(P), I32, I32, I32, P, ctypes.c_size_t]),
+        "fce_comm_group_create": (I32, [ctypes.POINTER(P), I32]),
+        "fce_comm_group_destroy": (I32, [P]),
+        "fce_comm_init_local": (I32, [ctypes.POINTER(P), P, I32, I32]),
         "fce_comm_destroy": (I32, [P]),
+        "fce_comm_query": (I32, [P, ctypes.POINTER(I32), ctypes.POINTER(I32), ctypes.POINTER(I32)]),
+        "fce_comm_scratch_bytes": (I32, [P, ctypes.POINTER(ctypes.c_size_t)]),
+        "fce_comm_all_gather": (I32, [P, P, P, P, ctypes.c_size_t]),
+        "fce_comm_all_reduce_f32": (I32, [P, P, P, P, ctypes.c_size_t]),
+        "fce_comm_reduce_scatter_f32": (I32, [P, P, P, P, ctypes.c_size_t]),
+        "fce_sp_gather": (I32, [P, P, P, I64, I64, I64, I64, P, I64]),
+        "fce_sp_scatter": (I32, [P, P, P, I64, I64, I64, P, I64, I64]),
+        "fce_dp_step": (I32, [P, P, ctypes.POINTER(FceProblem), I32, P, P, I64, P, I64]),
         "fce_vp_last_error": (ctypes.c_char_p, []),
         "fce_vp_forward": (I32, [P, P, ctypes.POINTER(FceProblem), I32, FceStats, P, P, P]),
         "fce_vp_backward": (I32, [P, P, ctypes.POINTER(FceProblem), FceStats, I32, F, P, P, I64, P, I64]),
@@ -330,7 +346,11 @@ def fused_backward_recompute(hidden, weight, targets, stats: Stats, reduction: s
                              dhidden=None, accumulate_dhidden: bool = False, grad_dtype=None):
     """Backward by logit recompute (fused_backward.hpp:118-140) -> (dH, dW), fp32
     by default; grad_dtype=torch.bfloat16 returns bf16 gradients (fce_backward_ex:
-    dW rounded straight from the accumulators, no fp32 V x D buffer)."""
+    dW rounded straight from the accumulators, no fp32 V x D buffer).
+
+    upstream (check_upstream, reduction.hpp:81-97): a Python number or a 0-d
+    tensor for mean / sum (a CUDA 0-d tensor is read on the device:
+    fce_backward_dev, no host sync), a length-N tensor for 'none'."""
     import torch
     if reduction not in REDUCTIONS:
         raise UnsupportedReduction(reduction)
@@ -338,18 +358,34 @@ def fused_backward_recompute(hidden, weight, targets, stats: Stats, reduction: s
     p, keep = make_problem(hidden, weight, targets, ignore_index)
     dev = hidden.device
     up_rows = None
+    up_dev = None
     up_scalar = 0.0
     if isinstance(upstream, (int, float)):
         up_scalar = float(upstream)
+    elif reduction != "none" and upstream.numel() == 1 and upstream.dim() == 0:
+        if upstream.is_cuda:
+            up_dev = upstream.to(device=dev, dtype=torch.float32).reshape(()).contiguous()
+        else:
+            up_scalar = float(upstream.item())
     else:
         up_rows = upstream.to(device=dev, dtype=torch.float32).contiguous()
+        if reduction == "none" and up_rows.numel() != p.n:
+            # reference check_upstream: a per-position upstream must cover every position
+            raise InconsistentUpstream(f"per-position upstream has {up_rows.numel()} entries, expected {p.n}")
     gdt = torch.float32 if grad_dtype is None else grad_dtype
     if gdt not in (torch.float32, torch.bfloat16):
         raise InvalidArgument("grad_dtype must be torch.float32 or torch.bfloat16")
     if dhidden is None and want_dhidden:
         dhidden = torch.empty(p.n, p.d, dtype=gdt, device=dev)
     dweight = torch.empty(p.v, p.d, dtype=gdt, device=dev) if want_dweight else None
-    if gdt == torch.float32 and (dhidden is None or dhidden.dtype == torch.float32):
+    if up_dev is not None:
+        code = {torch.float32: 0, torch.bfloat16: 1}
+        _check(h.lib.fce_backward_dev(h.raw, ctypes.byref(p), stats.c(), REDUCTIONS[reduction], _ptr(up_dev),
+                                      None, _ptr(dhidden), dhidden.stride(0) if dhidden is not None else 0,
+                                      code[dhidden.dtype] if dhidden is not None else 0,
+                                      _ptr(dweight), dweight.stride(0) if dweight is not None else 0,
+                                      code[gdt], 1 if accumulate_dhidden else 0))
+    elif gdt == torch.float32 and (dhidden is None or dhidden.dtype == torch.float32):
         _check(h.lib.fce_backward(h.raw, ctypes.byref(p), stats.c(), REDUCTIONS[reduction], up_scalar,
                                   _ptr(up_rows), _ptr(dhidden), dhidden.stride(0) if dhidden is not None else 0,
                                   _ptr(dweight), dweight.stride(0) if dweight is not None else 0,
@@ -472,8 +508,10 @@ def stream_stats(h_row, weight, target, lo: int, hi: int, handle=None) -> Stats:
         st = Stats.empty(1, dev)
         st.m.fill_(float("-inf")); st.a.zero_(); st.z_target.zero_(); st.found.zero_()
         return st
-    # a target outside the range (or none) never matches: use id hi
-    y = hi if target is None or target < 0 else int(target)
+    # a target outside the range (or none) never matches: use id hi (the
+    # reference's stream_stats never validates the target, it just reports
+    # found = false; fused_forward.hpp:137-154)
+    y = hi if target is None or not (lo <= int(target) < hi) else int(target)
     tv = torch.tensor([y], dtype=torch.int64, device=dev)
     return tp_rank_partial(h_row.reshape(1, d), weight[lo:hi], lo, max(hi + 1, weight.shape[0] + 1), tv,
                            None, handle)

@@ -74,10 +74,15 @@ struct fce_handle_s {
     struct Pending {
         int mode;
         cudaEvent_t start, stop;
-        double flops;
+        double flops;                 // total, or per live row when `live` is set
+        unsigned long long* live;     // pinned snapshot of the device live-row count (compacted problems)
     };
     std::vector<Pending> pending;
     std::vector<cudaEvent_t> event_pool;
+    cudaEvent_t switch_ev = nullptr;           // orders a new stream after the old one (fce_set_stream)
+    unsigned long long* live_host = nullptr;  // pinned slots for the live-row snapshots
+    int live_used = 0;
+    static constexpr int kLiveSlots = 1024;
     double k_ms[4] = {0, 0, 0, 0};
     double k_flops[4] = {0, 0, 0, 0};
     int64_t k_launches[4] = {0, 0, 0, 0};
@@ -280,39 +285,64 @@ cudaEvent_t pool_event(fce_handle h) {
     return e;
 }
 
-// Launches one tile kernel; with timing on, brackets it with CUDA events on
-// the handle's stream and records its algorithmic flop count.
-cudaError_t timed_launch(fce_handle h, const TileParams& p, const TensorMaps& maps, double flops,
-                         int fwd_variant = 0) {
-    cudaEvent_t e0 = nullptr, e1 = nullptr;
-    if (h->timing) {
-        e0 = pool_event(h);
-        e1 = pool_event(h);
-        cudaEventRecord(e0, h->stream);
-    }
-    cudaError_t e = fwd_variant == 1   ? launch_fwd_pair(p, maps, h->sms, h->stream)
-                    : fwd_variant == 2 ? launch_fwd_mc(p, maps, h->sms, h->stream)
-                                       : launch_tile_kernel(p, maps, h->sms, h->stream);
-    if (h->timing) {
-        cudaEventRecord(e1, h->stream);
-        h->pending.push_back({p.mode, e0, e1, flops});
-    }
-    h->launches += 1;
-    return e;
-}
-
 void drain_timing(fce_handle h) {
     for (auto& q : h->pending) {
         cudaEventSynchronize(q.stop);
         float ms = 0.f;
         cudaEventElapsedTime(&ms, q.start, q.stop);
         h->k_ms[q.mode] += ms;
-        h->k_flops[q.mode] += q.flops;
+        // compacted problems: algorithmic flops of the rows that were live
+        h->k_flops[q.mode] += q.live ? q.flops * static_cast<double>(*q.live) : q.flops;
         h->k_launches[q.mode] += 1;
         h->event_pool.push_back(q.start);
         h->event_pool.push_back(q.stop);
     }
     h->pending.clear();
+    h->live_used = 0;
+}
+
+// With timing on: events around the launch on the handle's stream and the
+// algorithmic flop count.  For a compacted problem (n_valid set) the count is
+// `flops_per_row` times the live-row count, which only the device knows: a
+// pinned snapshot of it is queued right after the launch and read when the
+// timing is drained.
+struct TimedRegion {
+    fce_handle h;
+    cudaEvent_t e0 = nullptr;
+    TimedRegion(fce_handle hh) : h(hh) {
+        if (h->timing) {
+            e0 = pool_event(h);
+            cudaEventRecord(e0, h->stream);
+        }
+    }
+    void done(int mode, double flops_total, double flops_per_row, const unsigned long long* n_valid) {
+        if (!h->timing) return;
+        cudaEvent_t e1 = pool_event(h);
+        cudaEventRecord(e1, h->stream);
+        unsigned long long* live = nullptr;
+        if (n_valid) {
+            if (!h->live_host && cudaMallocHost(&h->live_host, sizeof(unsigned long long) * h->kLiveSlots) != cudaSuccess)
+                h->live_host = nullptr;
+            if (h->live_host && h->live_used == h->kLiveSlots) drain_timing(h);
+            if (h->live_host) {
+                live = h->live_host + h->live_used++;
+                cudaMemcpyAsync(live, n_valid, sizeof(unsigned long long), cudaMemcpyDeviceToHost, h->stream);
+            }
+        }
+        h->pending.push_back({mode, e0, e1, live ? flops_per_row : flops_total, live});
+    }
+};
+
+// Launches one tile kernel (timed when timing is on).
+cudaError_t timed_launch(fce_handle h, const TileParams& p, const TensorMaps& maps, double flops,
+                         int fwd_variant = 0, double flops_per_row = 0, const unsigned long long* n_valid = nullptr) {
+    TimedRegion tr(h);
+    cudaError_t e = fwd_variant == 1   ? launch_fwd_pair(p, maps, h->sms, h->stream)
+                    : fwd_variant == 2 ? launch_fwd_mc(p, maps, h->sms, h->stream)
+                                       : launch_tile_kernel(p, maps, h->sms, h->stream);
+    tr.done(p.mode, flops, flops_per_row, n_valid);
+    h->launches += 1;
+    return e;
 }
 
 // Forward geometry: row blocks of 256 (CTA pairs) or 128 rows, and the
@@ -365,7 +395,8 @@ fce_status run_forward_tiles(fce_handle h, const fce_problem* p, const FwdGeom& 
     tp.part_a = pa;
     tp.part_zt = pzt;
     tp.part_found = pf;
-    cudaError_t e = timed_launch(h, tp, maps, 2.0 * p->n * p->d * p->v, g.pair ? 1 : g.mc ? 2 : 0);
+    cudaError_t e = timed_launch(h, tp, maps, 2.0 * p->n * p->d * p->v, g.pair ? 1 : g.mc ? 2 : 0,
+                                 2.0 * p->d * p->v, n_valid);
     if (e != cudaSuccess) return fail(FCE_CUDA_ERROR, "forward tile kernel: %s", cudaGetErrorString(e));
     return FCE_OK;
 }
@@ -467,18 +498,10 @@ fce_status run_backward_persistent(fce_handle h, const fce_problem* p, const flo
     }
     if (dw_bf16 && !(bp.tma_epi & 2))
         return fail(FCE_CUDA_ERROR, "bf16 dW needs the TMA epilogue (16-byte aligned rows)");
-    cudaEvent_t e0 = nullptr, e1 = nullptr;
-    if (h->timing) {
-        e0 = pool_event(h);
-        e1 = pool_event(h);
-        cudaEventRecord(e0, h->stream);
-    }
+    TimedRegion tr(h);
     cudaError_t e = launch_bwd_persistent(bp, maps, h->sms, h->stream);
-    if (h->timing) {
-        cudaEventRecord(e1, h->stream);
-        const double flops = 2.0 * p->n * p->d * p->v * (1 + (dhidden ? 1 : 0) + (dweight ? 1 : 0));
-        h->pending.push_back({3, e0, e1, flops});
-    }
+    const double per_row = 2.0 * p->d * p->v * (1 + (dhidden ? 1 : 0) + (dweight ? 1 : 0));
+    tr.done(3, per_row * p->n, per_row, n_valid);
     h->launches += 1;
     if (e != cudaSuccess) return fail(FCE_CUDA_ERROR, "persistent backward kernel: %s", cudaGetErrorString(e));
     return FCE_OK;
@@ -552,6 +575,8 @@ fce_status fce_destroy(fce_handle h) {
     cudaStreamSynchronize(h->stream);
     drain_timing(h);
     for (cudaEvent_t e : h->event_pool) cudaEventDestroy(e);
+    if (h->live_host) cudaFreeHost(h->live_host);
+    if (h->switch_ev) cudaEventDestroy(h->switch_ev);
     if (h->ws) cudaFree(h->ws);
     if (h->cws) cudaFree(h->cws);
     if (h->err) cudaFree(h->err);
@@ -562,7 +587,20 @@ fce_status fce_destroy(fce_handle h) {
 
 fce_status fce_set_stream(fce_handle h, void* stream) {
     if (!h) return fail(FCE_INVALID_ARGUMENT, "null handle");
-    h->stream = static_cast<cudaStream_t>(stream);
+    cudaStream_t ns = static_cast<cudaStream_t>(stream);
+    cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+    if (ns != h->stream) FCE_CUDA(cudaStreamIsCapturing(ns, &cap));
+    if (ns != h->stream && cap == cudaStreamCaptureStatusNone) {
+        // Work already queued on the old stream may still read or write the
+        // handle's workspaces and flag block: the new stream starts after it.
+        // (A stream under graph capture cannot wait on outside work; ordering
+        // a graph's launches is the caller's, as for any captured work.)
+        FCE_CUDA(cudaSetDevice(h->device));
+        if (!h->switch_ev) FCE_CUDA(cudaEventCreateWithFlags(&h->switch_ev, cudaEventDisableTiming));
+        FCE_CUDA(cudaEventRecord(h->switch_ev, h->stream));
+        FCE_CUDA(cudaStreamWaitEvent(ns, h->switch_ev, 0));
+    }
+    h->stream = ns;
     return FCE_OK;
 }
 
@@ -730,11 +768,23 @@ fce_status fce_merge_partials(fce_handle h, int parts, int64_t n, int64_t part_s
                               const uint8_t* found, const int64_t* targets, int32_t has_ignore,
                               int64_t ignore_index, int reduction, fce_stats merged, float* lse,
                               float* loss_rows, float* loss_reduced) {
+    return fce::merge_partials(h, parts, n, part_stride, part_stride, m, a, z_target, found, targets, has_ignore,
+                               ignore_index, reduction, merged, lse, loss_rows, loss_reduced);
+}
+
+}  // extern "C"
+
+namespace fce {
+
+fce_status merge_partials(fce_handle h, int parts, int64_t n, int64_t part_stride, int64_t found_stride,
+                          const float* m, const float* a, const float* z_target, const uint8_t* found,
+                          const int64_t* targets, int32_t has_ignore, int64_t ignore_index, int reduction,
+                          fce_stats merged, float* lse, float* loss_rows, float* loss_reduced) {
     fce_status s = check_handle(h);
     if (s) return s;
     if (parts <= 0) return fail(FCE_INVALID_LAYOUT, "no partials to merge");
     if (n <= 0) return fail(FCE_EMPTY_INPUT, "merge requires N > 0");
-    if (part_stride < n) return fail(FCE_DIMENSION_MISMATCH, "part stride smaller than N");
+    if (part_stride < n || found_stride < n) return fail(FCE_DIMENSION_MISMATCH, "part stride smaller than N");
     if (!m || !a || !z_target || !found || !targets) return fail(FCE_INVALID_ARGUMENT, "null partial");
     if (reduction < 0 || reduction > 2) return fail(FCE_UNSUPPORTED_REDUCTION, "unknown reduction %d", reduction);
     if ((s = reset_flags(h))) return s;
@@ -749,7 +799,7 @@ fce_status fce_merge_partials(fce_handle h, int parts, int64_t n, int64_t part_s
     int blocks = 0;
     e = launch_merge_stats(parts, n, part_stride, m, a, z_target, found, targets, has_ignore,
                            ignore_index, 1, merged.m, merged.a, merged.z_target, merged.found, lse,
-                           loss_rows, sc.ptr<double>(o_b), h->err, h->stream, &blocks);
+                           loss_rows, sc.ptr<double>(o_b), h->err, h->stream, &blocks, nullptr, found_stride);
     if (e != cudaSuccess) return fail(FCE_CUDA_ERROR, "merge kernel: %s", cudaGetErrorString(e));
     h->launches += 1;
     if (reduction != FCE_REDUCTION_NONE && loss_reduced) {
@@ -759,6 +809,10 @@ fce_status fce_merge_partials(fce_handle h, int parts, int64_t n, int64_t part_s
     }
     return read_errors(h, h->validate != 0);
 }
+
+}  // namespace fce
+
+extern "C" {
 
 static fce_status run_backward_tiles(fce_handle h, const fce_problem* p, const float* gamma,
                                      const float* lse, int64_t row_chunk, int64_t band, __nv_bfloat16* G,
@@ -772,10 +826,33 @@ fce_status fce_backward(fce_handle h, const fce_problem* p, fce_stats stats, int
                            dweight, lddw, FCE_DTYPE_F32, accumulate_dhidden);
 }
 
+static fce_status backward_impl(fce_handle h, const fce_problem* p, fce_stats stats, int reduction,
+                                float upstream_scalar, const float* upstream_dev, const float* upstream_rows,
+                                void* dhidden_out, int64_t lddh, int dh_dtype, void* dweight_out, int64_t lddw,
+                                int dw_dtype, int accumulate_dhidden);
+
 fce_status fce_backward_ex(fce_handle h, const fce_problem* p, fce_stats stats, int reduction,
                            float upstream_scalar, const float* upstream_rows, void* dhidden_out,
                            int64_t lddh, int dh_dtype, void* dweight_out, int64_t lddw, int dw_dtype,
                            int accumulate_dhidden) {
+    return backward_impl(h, p, stats, reduction, upstream_scalar, nullptr, upstream_rows, dhidden_out, lddh,
+                         dh_dtype, dweight_out, lddw, dw_dtype, accumulate_dhidden);
+}
+
+fce_status fce_backward_dev(fce_handle h, const fce_problem* p, fce_stats stats, int reduction,
+                            const float* upstream_scalar_dev, const float* upstream_rows, void* dhidden,
+                            int64_t lddh, int dh_dtype, void* dweight, int64_t lddw, int dw_dtype,
+                            int accumulate_dhidden) {
+    if (reduction != FCE_REDUCTION_NONE && !upstream_scalar_dev)
+        return fail(FCE_INCONSISTENT_UPSTREAM, "scalar reductions require the device upstream scalar");
+    return backward_impl(h, p, stats, reduction, 0.f, upstream_scalar_dev, upstream_rows, dhidden, lddh, dh_dtype,
+                         dweight, lddw, dw_dtype, accumulate_dhidden);
+}
+
+static fce_status backward_impl(fce_handle h, const fce_problem* p, fce_stats stats, int reduction,
+                                float upstream_scalar, const float* upstream_dev, const float* upstream_rows,
+                                void* dhidden_out, int64_t lddh, int dh_dtype, void* dweight_out, int64_t lddw,
+                                int dw_dtype, int accumulate_dhidden) {
     fce_status s = check_handle(h);
     if (s) return s;
     if ((s = check_problem(p))) return s;
@@ -884,7 +961,8 @@ fce_status fce_backward_ex(fce_handle h, const fce_problem* p, fce_stats stats, 
     }
 
     e = launch_gamma(p->n, p->targets, p->has_ignore, p->ignore_index, stats.m, stats.a, stats.found,
-                     reduction, upstream_scalar, upstream_rows, h->count, gamma, lse, h->err, h->stream);
+                     reduction, upstream_scalar, upstream_dev, upstream_rows, h->count, gamma, lse, h->err,
+                     h->stream);
     if (e != cudaSuccess) return fail(FCE_CUDA_ERROR, "gamma kernel: %s", cudaGetErrorString(e));
     h->launches += 1;
     if ((s = read_errors(h, h->validate != 0))) return s;

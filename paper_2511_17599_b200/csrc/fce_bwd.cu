@@ -758,13 +758,11 @@ constexpr int kBwdSmem = kPS * (kPA + kPB) + kEpiStage + 1024 + 512;
 
 cudaError_t launch_bwd_persistent(const BwdParams& p, const BwdMaps& maps, int grid,
                                   cudaStream_t stream) {
-    static bool attr_done[2] = {false, false};
     const int wide = p.epi_warps == 4 ? 0 : 1;
     auto kern = wide ? fce_bwd_persistent_kernel<8> : fce_bwd_persistent_kernel<4>;
-    if (!attr_done[wide]) {
-        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, kBwdSmem);
+    {
+        cudaError_t e = ensure_dyn_smem(reinterpret_cast<const void*>(kern), kBwdSmem);
         if (e != cudaSuccess) return e;
-        attr_done[wide] = true;
     }
     int pairs = grid / 2;
     if (pairs > p.units) pairs = p.units;

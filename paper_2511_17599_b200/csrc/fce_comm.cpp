@@ -1,0 +1,343 @@
+// Communicator transports behind fce_comm (see fce_comm.h).
+#include <dlfcn.h>
+#include <nccl.h>
+
+#include <algorithm>
+#include <chrono>
+#include <condition_variable>
+#include <cstdarg>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "fce_comm.h"
+#include "fce_internal.h"
+
+namespace fce {
+
+namespace {
+
+fce_status comm_fail(fce_status s, const char* fmt, ...) {
+    char buf[512];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, sizeof(buf), fmt, ap);
+    va_end(ap);
+    set_last_error(buf);
+    return s;
+}
+
+#define FCE_COMM_CUDA(call)                                                                       \
+    do {                                                                                          \
+        cudaError_t e_ = (call);                                                                  \
+        if (e_ != cudaSuccess)                                                                    \
+            return comm_fail(FCE_CUDA_ERROR, "%s failed: %s", #call, cudaGetErrorString(e_));     \
+    } while (0)
+
+// ------------------------------------------------------------------ NCCL
+struct NcclApi {
+    bool ok = false;
+    std::string why;
+    ncclResult_t (*get_unique_id)(ncclUniqueId*) = nullptr;
+    ncclResult_t (*comm_init_rank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
+    ncclResult_t (*comm_destroy)(ncclComm_t) = nullptr;
+    ncclResult_t (*all_gather)(const void*, void*, size_t, ncclDataType_t, ncclComm_t, cudaStream_t) = nullptr;
+    ncclResult_t (*all_reduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t,
+                               cudaStream_t) = nullptr;
+    ncclResult_t (*reduce_scatter)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t,
+                                   cudaStream_t) = nullptr;
+    const char* (*error_string)(ncclResult_t) = nullptr;
+};
+
+NcclApi& nccl() {
+    static NcclApi api;
+    static std::once_flag once;
+    std::call_once(once, [] {
+        void* lib = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+        if (!lib) lib = dlopen("libnccl.so", RTLD_NOW | RTLD_GLOBAL);
+        if (!lib) {
+            api.why = std::string("dlopen libnccl.so.2 failed: ") + dlerror();
+            return;
+        }
+#define FCE_SYM(field, name)                                              \
+    api.field = reinterpret_cast<decltype(api.field)>(dlsym(lib, name)); \
+    if (!api.field) {                                                     \
+        api.why = std::string("missing NCCL symbol ") + name;             \
+        return;                                                           \
+    }
+        FCE_SYM(get_unique_id, "ncclGetUniqueId");
+        FCE_SYM(comm_init_rank, "ncclCommInitRank");
+        FCE_SYM(comm_destroy, "ncclCommDestroy");
+        FCE_SYM(all_gather, "ncclAllGather");
+        FCE_SYM(all_reduce, "ncclAllReduce");
+        FCE_SYM(reduce_scatter, "ncclReduceScatter");
+        FCE_SYM(error_string, "ncclGetErrorString");
+#undef FCE_SYM
+        api.ok = true;
+    });
+    return api;
+}
+
+class NcclComm final : public Comm {
+public:
+    ncclComm_t comm = nullptr;
+    ~NcclComm() override {
+        if (comm && nccl().ok) nccl().comm_destroy(comm);
+    }
+    int transport() const override { return kTransportNccl; }
+    fce_status check(ncclResult_t r, const char* what) {
+        if (r == ncclSuccess) return FCE_OK;
+        return comm_fail(FCE_NCCL_ERROR, "%s: %s", what, nccl().error_string(r));
+    }
+    fce_status all_gather(const void* send, void* recv, size_t bytes, cudaStream_t s) override {
+        return check(nccl().all_gather(send, recv, bytes, ncclUint8, comm, s), "ncclAllGather");
+    }
+    fce_status all_reduce_sum(const float* send, float* recv, size_t count, cudaStream_t s) override {
+        return check(nccl().all_reduce(send, recv, count, ncclFloat32, ncclSum, comm, s), "ncclAllReduce");
+    }
+    fce_status reduce_scatter_sum(const float* send, float* recv, size_t recv_count, cudaStream_t s) override {
+        return check(nccl().reduce_scatter(send, recv, recv_count, ncclFloat32, ncclSum, comm, s),
+                     "ncclReduceScatter");
+    }
+};
+
+}  // namespace
+
+fce_status nccl_unique_id(uint8_t* out, size_t len) {
+    if (!out || len < sizeof(ncclUniqueId)) return comm_fail(FCE_INVALID_ARGUMENT, "id buffer too small");
+    NcclApi& api = nccl();
+    if (!api.ok) return comm_fail(FCE_NCCL_ERROR, "%s", api.why.c_str());
+    ncclUniqueId id;
+    ncclResult_t r = api.get_unique_id(&id);
+    if (r != ncclSuccess) return comm_fail(FCE_NCCL_ERROR, "ncclGetUniqueId: %s", api.error_string(r));
+    std::memcpy(out, &id, sizeof(id));
+    return FCE_OK;
+}
+
+fce_status make_nccl_comm(Comm** out, int device, int nranks, int rank, const uint8_t* id, size_t len) {
+    if (!id || len < sizeof(ncclUniqueId)) return comm_fail(FCE_INVALID_ARGUMENT, "bad NCCL id");
+    NcclApi& api = nccl();
+    if (!api.ok) return comm_fail(FCE_NCCL_ERROR, "%s", api.why.c_str());
+    FCE_COMM_CUDA(cudaSetDevice(device));
+    ncclUniqueId uid;
+    std::memcpy(&uid, id, sizeof(uid));
+    NcclComm* c = new NcclComm();
+    ncclResult_t r = api.comm_init_rank(&c->comm, nranks, uid, rank);
+    if (r != ncclSuccess) {
+        c->comm = nullptr;
+        delete c;
+        return comm_fail(FCE_NCCL_ERROR, "ncclCommInitRank: %s", api.error_string(r));
+    }
+    c->nranks = nranks;
+    c->rank = rank;
+    c->device = device;
+    *out = c;
+    return FCE_OK;
+}
+
+// ------------------------------------------------------------------ local
+// Rendezvous state shared by the k ranks of one in-process group.  Each
+// collective is a sequence of phases; in a phase every rank records an event
+// on its stream after the work the phase depends on, meets the others at a
+// host barrier, then makes its stream wait for every peer's event.  Device
+// work is never blocked on the host beyond the barrier itself.
+struct LocalGroup {
+    int nranks = 0;
+    std::mutex mu;
+    std::condition_variable cv;
+    int arrived = 0;
+    uint64_t gen = 0;
+    bool aborted = false;
+    int refs = 1;
+    std::vector<int> device;       // per rank, -1 until joined
+    std::vector<const void*> send; // published buffers of the current collective
+    std::vector<void*> recv;
+    std::vector<cudaEvent_t> ev;   // [phase][rank] published events
+    double timeout_s = 600.0;
+};
+
+namespace {
+
+constexpr int kPhases = 3;
+
+class LocalComm final : public Comm {
+public:
+    LocalGroup* g = nullptr;
+    cudaEvent_t ev[kPhases] = {nullptr, nullptr, nullptr};
+    bool peers_ready = false;
+
+    ~LocalComm() override {
+        for (cudaEvent_t e : ev)
+            if (e) cudaEventDestroy(e);
+        release_local_group(g);
+    }
+    int transport() const override { return kTransportLocal; }
+
+    fce_status barrier() {
+        std::unique_lock<std::mutex> lk(g->mu);
+        if (g->aborted) return comm_fail(FCE_NCCL_ERROR, "local communicator group was aborted by a peer");
+        const uint64_t my = g->gen;
+        if (++g->arrived == g->nranks) {
+            g->arrived = 0;
+            ++g->gen;
+            g->cv.notify_all();
+            return FCE_OK;
+        }
+        const bool ok = g->cv.wait_for(lk, std::chrono::duration<double>(g->timeout_s),
+                                       [&] { return g->gen != my || g->aborted; });
+        if (g->gen != my) return FCE_OK;
+        g->aborted = true;
+        g->cv.notify_all();
+        return comm_fail(FCE_NCCL_ERROR, ok ? "local communicator group aborted"
+                                            : "local collective timed out waiting for peer ranks "
+                                              "(every rank must call it, each from its own thread)");
+    }
+
+    // Record this rank's event for `phase`, meet the peers, wait for theirs.
+    fce_status sync_phase(int phase, cudaStream_t s) {
+        FCE_COMM_CUDA(cudaEventRecord(ev[phase], s));
+        {
+            std::lock_guard<std::mutex> lk(g->mu);
+            g->ev[phase * nranks + rank] = ev[phase];
+        }
+        fce_status st = barrier();
+        if (st) return st;
+        for (int q = 0; q < nranks; ++q)
+            if (q != rank) FCE_COMM_CUDA(cudaStreamWaitEvent(s, g->ev[phase * nranks + q], 0));
+        return FCE_OK;
+    }
+
+    void publish(const void* send, void* recv) {
+        std::lock_guard<std::mutex> lk(g->mu);
+        g->send[rank] = send;
+        g->recv[rank] = recv;
+    }
+
+    // Kernels of this rank read peers' buffers: peer access to every other device.
+    fce_status enable_peers() {
+        if (peers_ready) return FCE_OK;
+        for (int q = 0; q < nranks; ++q) {
+            const int pd = g->device[q];
+            if (pd == device || pd < 0) continue;
+            int can = 0;
+            FCE_COMM_CUDA(cudaDeviceCanAccessPeer(&can, device, pd));
+            if (!can) return comm_fail(FCE_NCCL_ERROR, "device %d cannot access peer device %d", device, pd);
+            cudaError_t e = cudaDeviceEnablePeerAccess(pd, 0);
+            if (e == cudaErrorPeerAccessAlreadyEnabled) {
+                cudaGetLastError();
+            } else if (e != cudaSuccess) {
+                return comm_fail(FCE_CUDA_ERROR, "cudaDeviceEnablePeerAccess(%d): %s", pd, cudaGetErrorString(e));
+            }
+        }
+        peers_ready = true;
+        return FCE_OK;
+    }
+
+    fce_status all_gather(const void* send, void* recv, size_t bytes, cudaStream_t s) override {
+        publish(send, recv);
+        fce_status st = sync_phase(0, s);
+        if (st) return st;
+        for (int q = 0; q < nranks; ++q) {
+            char* dst = static_cast<char*>(recv) + static_cast<size_t>(q) * bytes;
+            if (dst != g->send[q] && bytes)
+                FCE_COMM_CUDA(cudaMemcpyAsync(dst, g->send[q], bytes, cudaMemcpyDefault, s));
+        }
+        // peers may overwrite their send buffers only after everyone copied them
+        return sync_phase(1, s);
+    }
+
+    fce_status all_reduce_sum(const float* send, float* recv, size_t count, cudaStream_t s) override {
+        publish(send, recv);
+        fce_status st = sync_phase(0, s);
+        if (st) return st;
+        if ((st = enable_peers())) return st;
+        // reduce-scatter: rank r sums slice r of every rank's input into its own
+        // output (in place is safe: no peer reads slice r of this rank's buffer)
+        const size_t per = ((count + nranks - 1) / nranks + 3) / 4 * 4;
+        auto lo = [&](int q) { return std::min(count, static_cast<size_t>(q) * per); };
+        PeerPtrs src;
+        for (int q = 0; q < nranks; ++q) src.p[q] = static_cast<const float*>(g->send[q]) + lo(rank);
+        FCE_COMM_CUDA(launch_sum_peers(src, nranks, recv + lo(rank), lo(rank + 1) - lo(rank), s));
+        if ((st = sync_phase(1, s))) return st;
+        // all-gather of the reduced slices straight from the peers' outputs
+        for (int q = 0; q < nranks; ++q) {
+            if (q == rank || lo(q + 1) == lo(q)) continue;
+            FCE_COMM_CUDA(cudaMemcpyAsync(recv + lo(q), static_cast<float*>(g->recv[q]) + lo(q),
+                                          (lo(q + 1) - lo(q)) * sizeof(float), cudaMemcpyDefault, s));
+        }
+        return sync_phase(2, s);
+    }
+
+    fce_status reduce_scatter_sum(const float* send, float* recv, size_t recv_count, cudaStream_t s) override {
+        publish(send, recv);
+        fce_status st = sync_phase(0, s);
+        if (st) return st;
+        if ((st = enable_peers())) return st;
+        PeerPtrs src;
+        for (int q = 0; q < nranks; ++q)
+            src.p[q] = static_cast<const float*>(g->send[q]) + static_cast<size_t>(rank) * recv_count;
+        FCE_COMM_CUDA(launch_sum_peers(src, nranks, recv, recv_count, s));
+        return sync_phase(1, s);
+    }
+};
+
+}  // namespace
+
+fce_status make_local_group(LocalGroup** out, int nranks) {
+    if (!out) return comm_fail(FCE_INVALID_ARGUMENT, "null output");
+    if (nranks < 1 || nranks > kMaxLocalRanks)
+        return comm_fail(FCE_INVALID_LAYOUT, "local group size must be in [1, %d]", kMaxLocalRanks);
+    LocalGroup* g = new LocalGroup();
+    g->nranks = nranks;
+    g->device.assign(nranks, -1);
+    g->send.assign(nranks, nullptr);
+    g->recv.assign(nranks, nullptr);
+    g->ev.assign(kPhases * nranks, nullptr);
+    if (const char* t = std::getenv("FCE_LOCAL_TIMEOUT_S")) g->timeout_s = std::atof(t) > 0 ? std::atof(t) : 600.0;
+    *out = g;
+    return FCE_OK;
+}
+
+void release_local_group(LocalGroup* g) {
+    if (!g) return;
+    bool last;
+    {
+        std::lock_guard<std::mutex> lk(g->mu);
+        last = --g->refs == 0;
+    }
+    if (last) delete g;
+}
+
+fce_status make_local_comm(Comm** out, LocalGroup* g, int device, int rank) {
+    if (!out || !g) return comm_fail(FCE_INVALID_ARGUMENT, "null argument");
+    if (rank < 0 || rank >= g->nranks) return comm_fail(FCE_INVALID_LAYOUT, "rank %d outside [0, %d)", rank, g->nranks);
+    FCE_COMM_CUDA(cudaSetDevice(device));
+    LocalComm* c = new LocalComm();
+    for (auto& e : c->ev) {
+        cudaError_t err = cudaEventCreateWithFlags(&e, cudaEventDisableTiming);
+        if (err != cudaSuccess) {
+            delete c;  // g not yet referenced: c->g is null
+            return comm_fail(FCE_CUDA_ERROR, "cudaEventCreate: %s", cudaGetErrorString(err));
+        }
+    }
+    {
+        std::lock_guard<std::mutex> lk(g->mu);
+        if (g->device[rank] >= 0) {
+            delete c;
+            return comm_fail(FCE_INVALID_LAYOUT, "rank %d of the local group is already taken", rank);
+        }
+        g->device[rank] = device;
+        ++g->refs;
+    }
+    c->g = g;
+    c->nranks = g->nranks;
+    c->rank = rank;
+    c->device = device;
+    *out = c;
+    return FCE_OK;
+}
+
+}  // namespace fce

@@ -241,12 +241,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
 
 // p.m_blocks counts 256-row pairs here; grid = 2 x min(pairs on the device, units).
 cudaError_t launch_fwd_pair(const TileParams& p, const TensorMaps& maps, int sms, cudaStream_t stream) {
-    static bool attr_done = false;
-    if (!attr_done) {
-        cudaError_t e = cudaFuncSetAttribute(fce_fwd_pair_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                             kFwdPairSmem);
+    {
+        cudaError_t e = ensure_dyn_smem(reinterpret_cast<const void*>(fce_fwd_pair_kernel), kFwdPairSmem);
         if (e != cudaSuccess) return e;
-        attr_done = true;
     }
     int pairs = sms / 2;
     if (pairs > p.units) pairs = p.units;

@@ -113,6 +113,14 @@ cudaError_t launch_pair_gemm(const GemmProblem& q, const TensorMaps& maps, int s
 cudaError_t launch_bwd_persistent(const BwdParams& p, const BwdMaps& maps, int grid,
                                   cudaStream_t stream);
 
+// fce_merge_partials with a separate stride (in bytes) for the found flags, so
+// per-rank partials can travel as one packed block [m | a | z_t | found]
+// (fce_api.cpp).
+fce_status merge_partials(fce_handle h, int parts, int64_t n, int64_t part_stride, int64_t found_stride,
+                          const float* m, const float* a, const float* z_target, const uint8_t* found,
+                          const int64_t* targets, int32_t has_ignore, int64_t ignore_index, int reduction,
+                          fce_stats merged, float* lse, float* loss_rows, float* loss_reduced);
+
 // Stream a handle launches on (fce_api.cpp).
 cudaStream_t handle_stream(fce_handle h);
 // Thread-local message returned by fce_last_error (fce_api.cpp).
@@ -125,6 +133,10 @@ bool encode_map_2d(CUtensorMap* map, const void* base, uint64_t inner, uint64_t 
 cudaError_t launch_tile_kernel(const TileParams& p, const TensorMaps& maps, int grid,
                                cudaStream_t stream);
 int device_sm_count(int device);
+// One-time (per kernel and device, thread-safe) opt-in to `bytes` of dynamic
+// shared memory; several host threads may drive handles on the same or on
+// different devices (in-process communicator groups).
+cudaError_t ensure_dyn_smem(const void* func, int bytes);
 
 cudaError_t launch_prep_targets(const int64_t* targets, int64_t n, int has_ignore,
                                 int64_t ignore_index, int64_t v_total, int* err_flags,
@@ -134,7 +146,8 @@ cudaError_t launch_merge_stats(int parts, int64_t n, int64_t part_stride, const 
                                const int64_t* targets, int has_ignore, int64_t ignore_index,
                                int emit_loss, float* m, float* a, float* zt, uint8_t* found,
                                float* lse, float* loss_rows, double* block_sums, int* err_flags,
-                               cudaStream_t stream, int* blocks_out, const int* row_map = nullptr);
+                               cudaStream_t stream, int* blocks_out, const int* row_map = nullptr,
+                               int64_t found_stride = -1 /* -1: part_stride */);
 cudaError_t launch_round_to_bf16(const float* in, int64_t rows, int64_t cols, int64_t ld_in,
                                  __nv_bfloat16* out, int64_t ld_out, cudaStream_t stream);
 // ignored-row compaction (fce_kernels.cu)
@@ -153,7 +166,7 @@ cudaError_t launch_reduce_loss(const double* block_sums, int blocks,
                                float* loss_reduced, cudaStream_t stream);
 cudaError_t launch_gamma(int64_t n, const int64_t* targets, int has_ignore, int64_t ignore_index,
                          const float* m, const float* a, const uint8_t* found, int reduction,
-                         float upstream_scalar, const float* upstream_rows,
+                         float upstream_scalar, const float* upstream_dev, const float* upstream_rows,
                          const unsigned long long* valid_count, float* gamma, float* lse,
                          int* err_flags, cudaStream_t stream);
 cudaError_t launch_scale(float* x, int64_t count, const float* factor_dev, float factor,

@@ -26,6 +26,9 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
+#include <mutex>
+#include <set>
+#include <utility>
 #include <cudaTypedefs.h>
 
 #include "fce_internal.h"
@@ -406,16 +409,15 @@ __global__ void __launch_bounds__(kThreads, 1)
 // ============================================================== host helpers
 
 static PFN_cuTensorMapEncodeTiled_v12000 get_encode_fn() {
-    static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
-    if (!fn) {
+    // function-local static: initialised once, thread-safe
+    static const PFN_cuTensorMapEncodeTiled_v12000 fn = [] {
         cudaDriverEntryPointQueryResult q;
         void* ptr = nullptr;
-        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &ptr, cudaEnableDefault, &q) ==
-                cudaSuccess &&
-            q == cudaDriverEntryPointSuccess) {
-            fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(ptr);
-        }
-    }
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &ptr, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            return reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(ptr);
+        return static_cast<PFN_cuTensorMapEncodeTiled_v12000>(nullptr);
+    }();
     return fn;
 }
 
@@ -435,6 +437,19 @@ bool encode_map_2d(CUtensorMap* map, const void* base, uint64_t inner, uint64_t 
     return r == CUDA_SUCCESS;
 }
 
+cudaError_t ensure_dyn_smem(const void* func, int bytes) {
+    static std::mutex mu;
+    static std::set<std::pair<const void*, int>> done;
+    int dev = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return e;
+    std::lock_guard<std::mutex> lock(mu);
+    if (done.count({func, dev})) return cudaSuccess;
+    e = cudaFuncSetAttribute(func, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+    if (e == cudaSuccess) done.insert({func, dev});
+    return e;
+}
+
 int device_sm_count(int device) {
     int v = 0;
     cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, device);
@@ -444,12 +459,9 @@ int device_sm_count(int device) {
 template <int EPI>
 static cudaError_t launch_one(const TileParams& p, const TensorMaps& maps, int grid,
                               cudaStream_t stream) {
-    static bool attr_done = false;
-    if (!attr_done) {
-        cudaError_t e = cudaFuncSetAttribute(fce_tile_kernel<EPI, false>,
-                                             cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes);
+    {
+        cudaError_t e = ensure_dyn_smem(reinterpret_cast<const void*>(fce_tile_kernel<EPI, false>), kSmemBytes);
         if (e != cudaSuccess) return e;
-        attr_done = true;
     }
     fce_tile_kernel<EPI, false><<<grid, kThreads, kSmemBytes, stream>>>(p, maps);
     return cudaGetLastError();
@@ -458,12 +470,9 @@ static cudaError_t launch_one(const TileParams& p, const TensorMaps& maps, int g
 // Forward on 2-CTA clusters with W multicast (p.m_blocks counts row-block pairs).
 cudaError_t launch_fwd_mc(const TileParams& p, const TensorMaps& maps, int sms, cudaStream_t stream) {
     if (p.units <= 0) return cudaSuccess;
-    static bool attr_done = false;
-    if (!attr_done) {
-        cudaError_t e = cudaFuncSetAttribute(fce_tile_kernel<kEpiForward, true>,
-                                             cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes);
+    {
+        cudaError_t e = ensure_dyn_smem(reinterpret_cast<const void*>(fce_tile_kernel<kEpiForward, true>), kSmemBytes);
         if (e != cudaSuccess) return e;
-        attr_done = true;
     }
     int clusters = std::min(sms / 2, p.units);
     if (clusters < 1) clusters = 1;
@@ -525,7 +534,7 @@ cudaError_t launch_prep_targets(const int64_t* targets, int64_t n, int has_ignor
 // merge_stats (softmax_stats.hpp:52-75) applied in ascending part order
 // (fused_forward.hpp:112-123 for windows, parallel_sim.hpp:214-220 for
 // ranks), then loss = (m - z_t) + log a (softmax_stats.hpp:45).
-__global__ void k_merge_stats(int parts, int64_t n, int64_t stride, const float* __restrict__ pm,
+__global__ void k_merge_stats(int parts, int64_t n, int64_t stride, int64_t fstride, const float* __restrict__ pm,
                               const float* __restrict__ pa, const float* __restrict__ pzt,
                               const uint8_t* __restrict__ pf, const int64_t* __restrict__ targets,
                               int has_ignore, int64_t ignore_index, int emit_loss, float* m_out,
@@ -544,7 +553,7 @@ __global__ void k_merge_stats(int parts, int64_t n, int64_t stride, const float*
             for (int s = 0; s < parts; ++s) {
                 const int64_t o = s * stride + src;
                 const float sm = pm[o], sa = pa[o];
-                const bool sf = pf[o] != 0;
+                const bool sf = pf[s * fstride + src] != 0;
                 if (F && sf) atomicOr(&err[kErrDuplicate], 1);
                 const float nm = M > sm ? M : sm;
                 float acc = 0.f;
@@ -590,10 +599,12 @@ cudaError_t launch_merge_stats(int parts, int64_t n, int64_t part_stride, const 
                                const int64_t* targets, int has_ignore, int64_t ignore_index,
                                int emit_loss, float* m, float* a, float* zt, uint8_t* found,
                                float* lse, float* loss_rows, double* block_sums, int* err_flags,
-                               cudaStream_t stream, int* blocks_out, const int* row_map) {
+                               cudaStream_t stream, int* blocks_out, const int* row_map,
+                               int64_t found_stride) {
     const int blocks = static_cast<int>((n + 255) / 256);
     if (blocks_out) *blocks_out = blocks;
-    k_merge_stats<<<blocks, 256, 0, stream>>>(parts, n, part_stride, pm, pa, pzt, pf, targets,
+    k_merge_stats<<<blocks, 256, 0, stream>>>(parts, n, part_stride, found_stride >= 0 ? found_stride : part_stride,
+                                              pm, pa, pzt, pf, targets,
                                               has_ignore, ignore_index, emit_loss, m, a, zt, found,
                                               lse, loss_rows, block_sums, err_flags, row_map);
     return cudaGetLastError();
@@ -776,9 +787,9 @@ cudaError_t launch_reduce_loss(const double* block_sums, int blocks,
 __global__ void k_gamma(int64_t n, const int64_t* __restrict__ targets, int has_ignore,
                         int64_t ignore_index, const float* __restrict__ m,
                         const float* __restrict__ a, const uint8_t* __restrict__ found,
-                        int reduction, float upstream_scalar, const float* __restrict__ up_rows,
-                        const unsigned long long* valid_count, float* gamma, float* lse,
-                        int* err) {
+                        int reduction, float upstream_scalar, const float* __restrict__ up_dev,
+                        const float* __restrict__ up_rows, const unsigned long long* valid_count,
+                        float* gamma, float* lse, int* err) {
     const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (i >= n) return;
     const bool ign = has_ignore && targets[i] == ignore_index;
@@ -789,13 +800,15 @@ __global__ void k_gamma(int64_t n, const int64_t* __restrict__ targets, int has_
     }
     if (!(found[i] != 0) || !(a[i] > 0.f)) atomicOr(&err[kErrMissingStats], 1);
     float g;
+    // scalar upstream: by value, or read on the device (graph-capturable autograd)
+    const float up = up_dev ? *up_dev : upstream_scalar;
     if (reduction == 2) {
         g = up_rows[i];
     } else if (reduction == 0) {
         const unsigned long long c = *valid_count;
-        g = c > 0 ? upstream_scalar / static_cast<float>(c) : 0.f;
+        g = c > 0 ? up / static_cast<float>(c) : 0.f;
     } else {
-        g = upstream_scalar;
+        g = up;
     }
     gamma[i] = g;
     lse[i] = m[i] + logf(a[i]);
@@ -803,12 +816,12 @@ __global__ void k_gamma(int64_t n, const int64_t* __restrict__ targets, int has_
 
 cudaError_t launch_gamma(int64_t n, const int64_t* targets, int has_ignore, int64_t ignore_index,
                          const float* m, const float* a, const uint8_t* found, int reduction,
-                         float upstream_scalar, const float* upstream_rows,
+                         float upstream_scalar, const float* upstream_dev, const float* upstream_rows,
                          const unsigned long long* valid_count, float* gamma, float* lse,
                          int* err_flags, cudaStream_t stream) {
     const int blocks = static_cast<int>((n + 255) / 256);
     k_gamma<<<blocks, 256, 0, stream>>>(n, targets, has_ignore, ignore_index, m, a, found,
-                                        reduction, upstream_scalar, upstream_rows, valid_count,
+                                        reduction, upstream_scalar, upstream_dev, upstream_rows, valid_count,
                                         gamma, lse, err_flags);
     return cudaGetLastError();
 }

@@ -203,12 +203,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
 
 cudaError_t launch_pair_gemm(const GemmProblem& q, const TensorMaps& maps, int sms,
                              cudaStream_t stream) {
-    static bool attr_done = false;
-    if (!attr_done) {
-        cudaError_t e = cudaFuncSetAttribute(fce_pair_gemm_kernel,
-                                             cudaFuncAttributeMaxDynamicSharedMemorySize, kPairSmem);
+    {
+        cudaError_t e = ensure_dyn_smem(reinterpret_cast<const void*>(fce_pair_gemm_kernel), kPairSmem);
         if (e != cudaSuccess) return e;
-        attr_done = true;
     }
     const int units = ((q.m + 255) / 256) * ((q.n + 255) / 256);
     int pairs = sms / 2;

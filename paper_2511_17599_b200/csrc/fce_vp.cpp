@@ -1,76 +1,44 @@
-// Vocabulary-parallel split over k GPUs (one process per GPU).
+// Multi-rank entry points (include/fce/fce_vp.h) over the communicator
+// interface of fce_comm.h (NCCL or the in-process local transport).
 //
-// Replaces the in-process simulation of tp_forward / tp_backward
-// (reference proj/include/fusedce/parallel_sim.hpp:186-290) with real ranks:
-//   forward : fce_forward_partial on the local W shard (v_offset set), then
-//             ncclAllGather of the per-row (m, a, z_t, found) partials
-//             (16 B per row per rank) and a rank-ordered merge on every rank,
-//             so loss / lse / stats are identical everywhere.
-//   backward: fce_backward on the shard with the merged stats; dW stays local
-//             (parallel_sim.hpp:240-244), dH partials are summed with
-//             ncclAllReduce (parallel_sim.hpp:276-288).
-// NCCL is resolved with dlopen at first use, so a process that already
-// loaded torch's libnccl.so.2 shares that copy and the library carries no
-// link-time NCCL dependency.
-#include <dlfcn.h>
-#include <nccl.h>
-
+// Replaces the in-process simulation of the reference
+// (proj/include/fusedce/parallel_sim.hpp:158-378) with real ranks:
+//   fce_vp_forward  : fce_forward_partial on the local W shard (v_offset set),
+//                     one all-gather of the packed per-row (m, a, z_t, found)
+//                     block (13 B per row per rank) and a rank-ordered merge on
+//                     every rank (tp_forward, parallel_sim.hpp:186-236).
+//   fce_vp_backward : fce_backward on the shard with the merged stats; dW stays
+//                     local (parallel_sim.hpp:240-244), dH partials summed with
+//                     one all-reduce (parallel_sim.hpp:276-288).
+//   fce_sp_gather / fce_sp_scatter : the sequence-parallel <-> vocab-parallel
+//                     switch (sp_to_tp_gather, parallel_sim.hpp:294-314) as an
+//                     all-gather of H shards and a reduce-scatter of dH.
+//   fce_dp_step     : dp_step (parallel_sim.hpp:334-378): local fused step,
+//                     all-reduce of loss and dW, scaled by 1 / nranks.
+#include <algorithm>
 #include <cstdarg>
 #include <cstdio>
 #include <cstring>
-#include <mutex>
-#include <string>
+#include <vector>
 
 #include "../../include/fce/fce.h"
 #include "../../include/fce/fce_vp.h"
+#include "fce_comm.h"
 #include "fce_internal.h"
 
-namespace {
-
-struct NcclApi {
-    bool ok = false;
-    std::string why;
-    ncclResult_t (*get_unique_id)(ncclUniqueId*) = nullptr;
-    ncclResult_t (*comm_init_rank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
-    ncclResult_t (*comm_destroy)(ncclComm_t) = nullptr;
-    ncclResult_t (*all_gather)(const void*, void*, size_t, ncclDataType_t, ncclComm_t,
-                               cudaStream_t) = nullptr;
-    ncclResult_t (*all_reduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t,
-                               ncclComm_t, cudaStream_t) = nullptr;
-    ncclResult_t (*group_start)() = nullptr;
-    ncclResult_t (*group_end)() = nullptr;
-    const char* (*error_string)(ncclResult_t) = nullptr;
+struct fce_comm_s {
+    fce::Comm* impl = nullptr;
+    void* buf = nullptr;       // grow-only scratch (pack / gather buffers)
+    size_t buf_size = 0;
+    int64_t* xchg = nullptr;   // small exchange area: [4] send + [4 * nranks] recv
+    int64_t* xchg_host = nullptr;
 };
 
-NcclApi& nccl() {
-    static NcclApi api;
-    static std::once_flag once;
-    std::call_once(once, [] {
-        void* lib = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
-        if (!lib) lib = dlopen("libnccl.so", RTLD_NOW | RTLD_GLOBAL);
-        if (!lib) {
-            api.why = std::string("dlopen libnccl.so.2 failed: ") + dlerror();
-            return;
-        }
-#define FCE_SYM(field, name)                                                 \
-    api.field = reinterpret_cast<decltype(api.field)>(dlsym(lib, name));    \
-    if (!api.field) {                                                        \
-        api.why = std::string("missing NCCL symbol ") + name;                \
-        return;                                                              \
-    }
-        FCE_SYM(get_unique_id, "ncclGetUniqueId");
-        FCE_SYM(comm_init_rank, "ncclCommInitRank");
-        FCE_SYM(comm_destroy, "ncclCommDestroy");
-        FCE_SYM(all_gather, "ncclAllGather");
-        FCE_SYM(all_reduce, "ncclAllReduce");
-        FCE_SYM(group_start, "ncclGroupStart");
-        FCE_SYM(group_end, "ncclGroupEnd");
-        FCE_SYM(error_string, "ncclGetErrorString");
-#undef FCE_SYM
-        api.ok = true;
-    });
-    return api;
-}
+struct fce_comm_group_s {
+    fce::LocalGroup* g = nullptr;
+};
+
+namespace {
 
 fce_status vp_fail(fce_status s, const char* fmt, ...) {
     char buf[512];
@@ -82,124 +50,341 @@ fce_status vp_fail(fce_status s, const char* fmt, ...) {
     return s;
 }
 
-}  // namespace
+#define VP_CUDA(call)                                                                             \
+    do {                                                                                          \
+        cudaError_t e_ = (call);                                                                  \
+        if (e_ != cudaSuccess)                                                                    \
+            return vp_fail(FCE_CUDA_ERROR, "%s failed: %s", #call, cudaGetErrorString(e_));       \
+    } while (0)
 
-struct fce_comm_s {
-    ncclComm_t comm = nullptr;
-    int nranks = 1;
-    int rank = 0;
-    // gather buffers, grown on demand
-    void* buf = nullptr;
-    size_t buf_size = 0;
-};
+size_t round_up(size_t a, size_t b) { return (a + b - 1) / b * b; }
+
+// Grow-only scratch of the communicator.  Peers of the local transport read
+// this rank's buffers only inside a collective, which ends with this stream
+// waiting for their reads, so a stream sync makes the old buffer free.
+fce_status scratch(fce_comm c, size_t bytes, cudaStream_t s, char** out) {
+    if (bytes > c->buf_size) {
+        if (c->buf) {
+            VP_CUDA(cudaStreamSynchronize(s));
+            cudaFree(c->buf);
+            c->buf = nullptr;
+            c->buf_size = 0;
+        }
+        VP_CUDA(cudaMalloc(&c->buf, bytes));
+        c->buf_size = bytes;
+    }
+    *out = static_cast<char*>(c->buf);
+    return FCE_OK;
+}
+
+fce_status finish_comm_init(fce_comm c) {
+    const size_t bytes = sizeof(int64_t) * 4 * (1 + static_cast<size_t>(c->impl->nranks));
+    VP_CUDA(cudaMalloc(&c->xchg, bytes));
+    VP_CUDA(cudaMallocHost(&c->xchg_host, bytes));
+    return FCE_OK;
+}
+
+// All-gather of up to 4 int64 per rank through the device (host sync):
+// out[r * 4 + i] = rank r's vals[i].
+fce_status exchange(fce_comm c, cudaStream_t s, const int64_t* vals, int cnt, std::vector<int64_t>* out) {
+    const int k = c->impl->nranks;
+    int64_t* host = c->xchg_host;
+    for (int i = 0; i < 4; ++i) host[i] = i < cnt ? vals[i] : 0;
+    VP_CUDA(cudaMemcpyAsync(c->xchg, host, 4 * sizeof(int64_t), cudaMemcpyHostToDevice, s));
+    fce_status st = c->impl->all_gather(c->xchg, c->xchg + 4, 4 * sizeof(int64_t), s);
+    if (st) return st;
+    VP_CUDA(cudaMemcpyAsync(host + 4, c->xchg + 4, 4 * sizeof(int64_t) * k, cudaMemcpyDeviceToHost, s));
+    VP_CUDA(cudaStreamSynchronize(s));
+    out->assign(host + 4, host + 4 + 4 * k);
+    return FCE_OK;
+}
+
+fce_status check_args(fce_handle h, fce_comm c) {
+    if (!h || !c || !c->impl) return vp_fail(FCE_INVALID_ARGUMENT, "null handle or communicator");
+    return FCE_OK;
+}
+
+// dst[rows, ld_dst] (+ tight copy) of a row-major block of `row_bytes` per row.
+fce_status copy_rows(void* dst, size_t ld_dst_bytes, const void* src, size_t ld_src_bytes, size_t row_bytes,
+                     size_t rows, cudaStream_t s) {
+    if (!rows || !row_bytes) return FCE_OK;
+    VP_CUDA(cudaMemcpy2DAsync(dst, ld_dst_bytes, src, ld_src_bytes, row_bytes, rows, cudaMemcpyDeviceToDevice, s));
+    return FCE_OK;
+}
+
+}  // namespace
 
 extern "C" {
 
 const char* fce_vp_last_error(void) { return fce_last_error(); }
 
-fce_status fce_comm_unique_id(uint8_t* out, size_t len) {
-    if (!out || len < sizeof(ncclUniqueId)) return vp_fail(FCE_INVALID_ARGUMENT, "id buffer too small");
-    NcclApi& api = nccl();
-    if (!api.ok) return vp_fail(FCE_NCCL_ERROR, "%s", api.why.c_str());
-    ncclUniqueId id;
-    ncclResult_t r = api.get_unique_id(&id);
-    if (r != ncclSuccess) return vp_fail(FCE_NCCL_ERROR, "ncclGetUniqueId: %s", api.error_string(r));
-    std::memcpy(out, &id, sizeof(id));
+fce_status fce_comm_unique_id(uint8_t* out, size_t len) { return fce::nccl_unique_id(out, len); }
+
+fce_status fce_comm_init(fce_comm* out, int device, int nranks, int rank, const uint8_t* id, size_t len) {
+    if (!out) return vp_fail(FCE_INVALID_ARGUMENT, "null output");
+    *out = nullptr;
+    if (nranks < 1 || rank < 0 || rank >= nranks) return vp_fail(FCE_INVALID_LAYOUT, "bad rank layout");
+    fce::Comm* impl = nullptr;
+    fce_status s = fce::make_nccl_comm(&impl, device, nranks, rank, id, len);
+    if (s) return s;
+    fce_comm c = new fce_comm_s();
+    c->impl = impl;
+    if ((s = finish_comm_init(c))) {
+        fce_comm_destroy(c);
+        return s;
+    }
+    *out = c;
     return FCE_OK;
 }
 
-fce_status fce_comm_init(fce_comm* out, int device, int nranks, int rank, const uint8_t* id,
-                         size_t len) {
-    if (!out || !id || len < sizeof(ncclUniqueId)) return vp_fail(FCE_INVALID_ARGUMENT, "bad arguments");
-    if (nranks < 1 || rank < 0 || rank >= nranks) return vp_fail(FCE_INVALID_LAYOUT, "bad rank layout");
-    NcclApi& api = nccl();
-    if (!api.ok) return vp_fail(FCE_NCCL_ERROR, "%s", api.why.c_str());
-    if (cudaSetDevice(device) != cudaSuccess) return vp_fail(FCE_CUDA_ERROR, "cudaSetDevice failed");
-    ncclUniqueId uid;
-    std::memcpy(&uid, id, sizeof(uid));
+fce_status fce_comm_group_create(fce_comm_group* out, int nranks) {
+    if (!out) return vp_fail(FCE_INVALID_ARGUMENT, "null output");
+    fce::LocalGroup* g = nullptr;
+    fce_status s = fce::make_local_group(&g, nranks);
+    if (s) return s;
+    *out = new fce_comm_group_s{g};
+    return FCE_OK;
+}
+
+fce_status fce_comm_group_destroy(fce_comm_group g) {
+    if (!g) return FCE_OK;
+    fce::release_local_group(g->g);
+    delete g;
+    return FCE_OK;
+}
+
+fce_status fce_comm_init_local(fce_comm* out, fce_comm_group g, int device, int rank) {
+    if (!out || !g) return vp_fail(FCE_INVALID_ARGUMENT, "null argument");
+    *out = nullptr;
+    fce::Comm* impl = nullptr;
+    fce_status s = fce::make_local_comm(&impl, g->g, device, rank);
+    if (s) return s;
     fce_comm c = new fce_comm_s();
-    ncclResult_t r = api.comm_init_rank(&c->comm, nranks, uid, rank);
-    if (r != ncclSuccess) {
-        delete c;
-        return vp_fail(FCE_NCCL_ERROR, "ncclCommInitRank: %s", api.error_string(r));
+    c->impl = impl;
+    if ((s = finish_comm_init(c))) {
+        fce_comm_destroy(c);
+        return s;
     }
-    c->nranks = nranks;
-    c->rank = rank;
     *out = c;
     return FCE_OK;
 }
 
 fce_status fce_comm_destroy(fce_comm c) {
     if (!c) return FCE_OK;
-    if (c->comm && nccl().ok) nccl().comm_destroy(c->comm);
+    if (c->impl) cudaSetDevice(c->impl->device);
     if (c->buf) cudaFree(c->buf);
+    if (c->xchg) cudaFree(c->xchg);
+    if (c->xchg_host) cudaFreeHost(c->xchg_host);
+    delete c->impl;
     delete c;
     return FCE_OK;
 }
 
-fce_status fce_vp_forward(fce_handle h, fce_comm c, const fce_problem* p, int reduction,
-                          fce_stats merged, float* lse, float* loss_rows, float* loss_reduced) {
-    if (!h || !c || !p) return vp_fail(FCE_INVALID_ARGUMENT, "null argument");
-    const int64_t n = p->n;
-    const size_t per_rank = (3 * sizeof(float) + 1) * static_cast<size_t>(n);
-    const size_t need = 2 * per_rank * static_cast<size_t>(c->nranks) + 1024;
-    if (need > c->buf_size) {
-        if (c->buf) cudaFree(c->buf);
-        c->buf = nullptr;
-        if (cudaMalloc(&c->buf, need) != cudaSuccess) return vp_fail(FCE_CUDA_ERROR, "gather buffer");
-        c->buf_size = need;
-    }
-    char* base = static_cast<char*>(c->buf);
-    // local partial: [m | a | zt] floats then found bytes
-    float* lm = reinterpret_cast<float*>(base);
-    float* la = lm + n;
-    float* lz = la + n;
-    uint8_t* lf = reinterpret_cast<uint8_t*>(lz + n);
-    char* gbase = base + ((per_rank + 255) & ~size_t(255));
-    float* gm = reinterpret_cast<float*>(gbase);
-    float* ga = gm + n * c->nranks;
-    float* gz = ga + n * c->nranks;
-    uint8_t* gf = reinterpret_cast<uint8_t*>(gz + n * c->nranks);
-
-    fce_stats part{lm, la, lz, lf};
-    fce_status s = fce_forward_partial(h, p, part);
-    if (s) return s;
-    // collectives run on the handle's stream, ordered after the partial kernels
-    cudaStream_t stream = fce::handle_stream(h);
-    NcclApi& api = nccl();
-    api.group_start();
-    api.all_gather(lm, gm, n, ncclFloat32, c->comm, stream);
-    api.all_gather(la, ga, n, ncclFloat32, c->comm, stream);
-    api.all_gather(lz, gz, n, ncclFloat32, c->comm, stream);
-    api.all_gather(lf, gf, n, ncclUint8, c->comm, stream);
-    ncclResult_t r = api.group_end();
-    if (r != ncclSuccess) return vp_fail(FCE_NCCL_ERROR, "all-gather of stats: %s", api.error_string(r));
-    return fce_merge_partials(h, c->nranks, n, n, gm, ga, gz, gf, p->targets, p->has_ignore,
-                              p->ignore_index, reduction, merged, lse, loss_rows, loss_reduced);
+fce_status fce_comm_query(fce_comm c, int* nranks, int* rank, int* transport) {
+    if (!c || !c->impl) return vp_fail(FCE_INVALID_ARGUMENT, "null communicator");
+    if (nranks) *nranks = c->impl->nranks;
+    if (rank) *rank = c->impl->rank;
+    if (transport) *transport = c->impl->transport();
+    return FCE_OK;
 }
 
-fce_status fce_vp_backward(fce_handle h, fce_comm c, const fce_problem* p, fce_stats merged,
-                           int reduction, float upstream_scalar, const float* upstream_rows,
-                           float* dhidden, int64_t lddh, float* dweight_shard, int64_t lddw) {
-    if (!h || !c || !p) return vp_fail(FCE_INVALID_ARGUMENT, "null argument");
-    fce_status s = fce_backward(h, p, merged, reduction, upstream_scalar, upstream_rows, dhidden,
-                                lddh, dweight_shard, lddw, 0);
+fce_status fce_comm_scratch_bytes(fce_comm c, size_t* bytes) {
+    if (!c || !bytes) return vp_fail(FCE_INVALID_ARGUMENT, "null argument");
+    *bytes = c->buf_size;
+    return FCE_OK;
+}
+
+fce_status fce_comm_all_gather(fce_handle h, fce_comm c, const void* send, void* recv, size_t bytes_per_rank) {
+    fce_status s = check_args(h, c);
     if (s) return s;
-    if (!dhidden || c->nranks == 1) return FCE_OK;
+    return c->impl->all_gather(send, recv, bytes_per_rank, fce::handle_stream(h));
+}
+
+fce_status fce_comm_all_reduce_f32(fce_handle h, fce_comm c, const float* send, float* recv, size_t count) {
+    fce_status s = check_args(h, c);
+    if (s) return s;
+    return c->impl->all_reduce_sum(send, recv, count, fce::handle_stream(h));
+}
+
+fce_status fce_comm_reduce_scatter_f32(fce_handle h, fce_comm c, const float* send, float* recv,
+                                       size_t recv_count) {
+    fce_status s = check_args(h, c);
+    if (s) return s;
+    return c->impl->reduce_scatter_sum(send, recv, recv_count, fce::handle_stream(h));
+}
+
+fce_status fce_vp_forward(fce_handle h, fce_comm c, const fce_problem* p, int reduction, fce_stats merged,
+                          float* lse, float* loss_rows, float* loss_reduced) {
+    fce_status s = check_args(h, c);
+    if (s) return s;
+    if (!p) return vp_fail(FCE_INVALID_ARGUMENT, "null problem");
+    if (p->n <= 0) return vp_fail(FCE_EMPTY_INPUT, "tp forward requires N > 0 and d > 0");
+    const int k = c->impl->nranks;
+    const int64_t n = p->n;
     cudaStream_t stream = fce::handle_stream(h);
-    NcclApi& api = nccl();
-    ncclResult_t r;
-    if (lddh == p->d) {
-        r = api.all_reduce(dhidden, dhidden, static_cast<size_t>(p->n * p->d), ncclFloat32, ncclSum,
-                           c->comm, stream);
-    } else {
-        api.group_start();
-        for (int64_t i = 0; i < p->n; ++i)
-            api.all_reduce(dhidden + i * lddh, dhidden + i * lddh, static_cast<size_t>(p->d),
-                           ncclFloat32, ncclSum, c->comm, stream);
-        r = api.group_end();
+    // per rank: [m (n f32) | a (n f32) | z_t (n f32) | found (n u8)], 256-byte aligned
+    const size_t rank_bytes = round_up(13 * static_cast<size_t>(n), 256);
+    char* buf = nullptr;
+    if ((s = scratch(c, rank_bytes * (1 + static_cast<size_t>(k)), stream, &buf))) return s;
+    float* lm = reinterpret_cast<float*>(buf);
+    fce_stats part{lm, lm + n, lm + 2 * n, reinterpret_cast<uint8_t*>(buf + 12 * n)};
+    if ((s = fce_forward_partial(h, p, part))) return s;
+    char* g = buf + rank_bytes;
+    if ((s = c->impl->all_gather(buf, g, rank_bytes, stream))) return s;
+    const float* gm = reinterpret_cast<const float*>(g);
+    return fce::merge_partials(h, k, n, static_cast<int64_t>(rank_bytes / 4), static_cast<int64_t>(rank_bytes), gm,
+                               gm + n, gm + 2 * n, reinterpret_cast<const uint8_t*>(g + 12 * n), p->targets,
+                               p->has_ignore, p->ignore_index, reduction, merged, lse, loss_rows, loss_reduced);
+}
+
+fce_status fce_vp_backward(fce_handle h, fce_comm c, const fce_problem* p, fce_stats merged, int reduction,
+                           float upstream_scalar, const float* upstream_rows, float* dhidden, int64_t lddh,
+                           float* dweight_shard, int64_t lddw) {
+    fce_status s = check_args(h, c);
+    if (s) return s;
+    if (!p) return vp_fail(FCE_INVALID_ARGUMENT, "null problem");
+    if (!dhidden)
+        return fce_backward(h, p, merged, reduction, upstream_scalar, upstream_rows, nullptr, 0, dweight_shard,
+                            lddw, 0);
+    if (lddh < p->d) return vp_fail(FCE_DIMENSION_MISMATCH, "lddh < d");
+    cudaStream_t stream = fce::handle_stream(h);
+    // a strided dH is reduced through a packed [n, d] buffer (one collective)
+    float* dst = dhidden;
+    if (lddh != p->d) {
+        char* buf = nullptr;
+        if ((s = scratch(c, sizeof(float) * static_cast<size_t>(p->n) * p->d, stream, &buf))) return s;
+        dst = reinterpret_cast<float*>(buf);
     }
-    if (r != ncclSuccess) return vp_fail(FCE_NCCL_ERROR, "all-reduce of dH: %s", api.error_string(r));
+    if ((s = fce_backward(h, p, merged, reduction, upstream_scalar, upstream_rows, dst, p->d, dweight_shard, lddw,
+                          0)))
+        return s;
+    if ((s = c->impl->all_reduce_sum(dst, dst, static_cast<size_t>(p->n) * p->d, stream))) return s;
+    if (dst != dhidden)
+        return copy_rows(dhidden, sizeof(float) * lddh, dst, sizeof(float) * p->d, sizeof(float) * p->d, p->n,
+                         stream);
+    return FCE_OK;
+}
+
+fce_status fce_sp_gather(fce_handle h, fce_comm c, const void* shard, int64_t shard_rows, int64_t ld_shard,
+                         int64_t d, int64_t n_total, void* full, int64_t ld_full) {
+    fce_status s = check_args(h, c);
+    if (s) return s;
+    if (d <= 0 || n_total <= 0) return vp_fail(FCE_EMPTY_INPUT, "sp gather requires d > 0 and N > 0");
+    if (shard_rows < 0 || (shard_rows > 0 && (!shard || ld_shard < d)) || !full || ld_full < d)
+        return vp_fail(FCE_INVALID_ARGUMENT, "bad shard / output buffers");
+    const int k = c->impl->nranks;
+    cudaStream_t stream = fce::handle_stream(h);
+    std::vector<int64_t> all;
+    const int64_t mine[2] = {shard_rows, d};
+    if ((s = exchange(c, stream, mine, 2, &all))) return s;
+    int64_t total = 0, rows_max = 0;
+    for (int q = 0; q < k; ++q) {
+        if (all[4 * q + 1] != d) return vp_fail(FCE_INVALID_LAYOUT, "hidden shards disagree on width");
+        total += all[4 * q];
+        rows_max = std::max(rows_max, all[4 * q]);
+    }
+    if (total != n_total)
+        return vp_fail(FCE_DIMENSION_MISMATCH, "shard rows add up to %lld, not N = %lld", (long long)total,
+                       (long long)n_total);
+    const size_t row_b = sizeof(uint16_t) * d;
+    const size_t blk = round_up(row_b * rows_max, 256);
+    char* buf = nullptr;
+    if ((s = scratch(c, blk * (1 + static_cast<size_t>(k)), stream, &buf))) return s;
+    if ((s = copy_rows(buf, row_b, shard, sizeof(uint16_t) * ld_shard, row_b, shard_rows, stream))) return s;
+    if ((s = c->impl->all_gather(buf, buf + blk, blk, stream))) return s;
+    int64_t at = 0;
+    for (int q = 0; q < k; ++q) {
+        if ((s = copy_rows(static_cast<char*>(full) + sizeof(uint16_t) * ld_full * at, sizeof(uint16_t) * ld_full,
+                           buf + blk * (1 + q), row_b, row_b, all[4 * q], stream)))
+            return s;
+        at += all[4 * q];
+    }
+    return FCE_OK;
+}
+
+fce_status fce_sp_scatter(fce_handle h, fce_comm c, const float* dh_partial, int64_t n_total, int64_t lddh,
+                          int64_t d, float* dh_shard, int64_t shard_rows, int64_t ld_shard) {
+    fce_status s = check_args(h, c);
+    if (s) return s;
+    if (d <= 0 || n_total <= 0) return vp_fail(FCE_EMPTY_INPUT, "sp scatter requires d > 0 and N > 0");
+    if (!dh_partial || lddh < d || shard_rows < 0 || (shard_rows > 0 && (!dh_shard || ld_shard < d)))
+        return vp_fail(FCE_INVALID_ARGUMENT, "bad dH / shard buffers");
+    const int k = c->impl->nranks, r = c->impl->rank;
+    cudaStream_t stream = fce::handle_stream(h);
+    std::vector<int64_t> all;
+    const int64_t mine[2] = {shard_rows, d};
+    if ((s = exchange(c, stream, mine, 2, &all))) return s;
+    int64_t total = 0, rows_max = 0;
+    for (int q = 0; q < k; ++q) {
+        if (all[4 * q + 1] != d) return vp_fail(FCE_INVALID_LAYOUT, "dH shards disagree on width");
+        total += all[4 * q];
+        rows_max = std::max(rows_max, all[4 * q]);
+    }
+    if (total != n_total)
+        return vp_fail(FCE_DIMENSION_MISMATCH, "shard rows add up to %lld, not N = %lld", (long long)total,
+                       (long long)n_total);
+    // send: [k][rows_max][d] with block q = rows of rank q's shard (zero padded)
+    const size_t row_b = sizeof(float) * d;
+    const size_t blk_elems = round_up(static_cast<size_t>(rows_max) * d, 64);
+    char* buf = nullptr;
+    if ((s = scratch(c, sizeof(float) * blk_elems * (1 + static_cast<size_t>(k)), stream, &buf))) return s;
+    float* send = reinterpret_cast<float*>(buf);
+    float* recv = send + blk_elems * k;
+    VP_CUDA(cudaMemsetAsync(send, 0, sizeof(float) * blk_elems * k, stream));
+    int64_t at = 0;
+    for (int q = 0; q < k; ++q) {
+        if ((s = copy_rows(send + blk_elems * q, row_b, dh_partial + at * lddh, sizeof(float) * lddh, row_b,
+                           all[4 * q], stream)))
+            return s;
+        at += all[4 * q];
+    }
+    if ((s = c->impl->reduce_scatter_sum(send, recv, blk_elems, stream))) return s;
+    return copy_rows(dh_shard, sizeof(float) * ld_shard, recv, row_b, row_b, all[4 * r], stream);
+}
+
+fce_status fce_dp_step(fce_handle h, fce_comm c, const fce_problem* p, int reduction, float* loss, float* dhidden,
+                       int64_t lddh, float* dweight, int64_t lddw) {
+    fce_status s = check_args(h, c);
+    if (s) return s;
+    if (!p || !loss || !dweight) return vp_fail(FCE_INVALID_ARGUMENT, "null problem, loss or dW");
+    if (reduction == FCE_REDUCTION_NONE)
+        return vp_fail(FCE_UNSUPPORTED_REDUCTION, "data-parallel loss sync requires a scalar reduction");
+    if (reduction != FCE_REDUCTION_MEAN && reduction != FCE_REDUCTION_SUM)
+        return vp_fail(FCE_UNSUPPORTED_REDUCTION, "unknown reduction %d", reduction);
+    if (lddw < p->d) return vp_fail(FCE_DIMENSION_MISMATCH, "lddw < d");
+    const int k = c->impl->nranks;
+    cudaStream_t stream = fce::handle_stream(h);
+    std::vector<int64_t> all;
+    const int64_t mine[3] = {p->n, p->d, p->v};
+    if ((s = exchange(c, stream, mine, 3, &all))) return s;
+    for (int q = 0; q < k; ++q) {
+        if (all[4 * q] != p->n) return vp_fail(FCE_INVALID_LAYOUT, "replica micro-batches must have equal sizes");
+        if (all[4 * q + 1] != p->d || all[4 * q + 2] != p->v)
+            return vp_fail(FCE_DIMENSION_MISMATCH, "replicas disagree on the weight shape");
+    }
+    const size_t n = static_cast<size_t>(std::max<int64_t>(p->n, 1));
+    // scratch: stats (13 B / row) + lse + per-row loss, then (strided dW) a packed dW
+    const size_t rows_off = round_up(17 * n, 16);
+    const size_t st_b = round_up(rows_off + 4 * n, 256);
+    const size_t dw_b = lddw != p->d ? sizeof(float) * static_cast<size_t>(p->v) * p->d : 0;
+    char* buf = nullptr;
+    if ((s = scratch(c, st_b + dw_b, stream, &buf))) return s;
+    float* fm = reinterpret_cast<float*>(buf);
+    fce_stats st{fm, fm + n, fm + 2 * n, reinterpret_cast<uint8_t*>(fm + 4 * n)};
+    float* lse = fm + 3 * n;
+    float* rows = reinterpret_cast<float*>(buf + rows_off);
+    if ((s = fce_forward(h, p, reduction, 0, st, lse, rows, loss))) return s;
+    float* dw = dw_b ? reinterpret_cast<float*>(buf + st_b) : dweight;
+    if ((s = fce_backward(h, p, st, reduction, 1.0f, nullptr, dhidden, lddh, dw, p->d, 0))) return s;
+    // loss and dW: mean over replicas (sum in rank order, then x 1 / nranks)
+    const size_t dw_count = static_cast<size_t>(p->v) * p->d;
+    if ((s = c->impl->all_reduce_sum(loss, loss, 1, stream))) return s;
+    if ((s = c->impl->all_reduce_sum(dw, dw, dw_count, stream))) return s;
+    const float inv = 1.0f / static_cast<float>(k);
+    if ((s = fce_scale(h, loss, 1, inv))) return s;
+    if ((s = fce_scale(h, dw, static_cast<int64_t>(dw_count), inv))) return s;
+    if (dw != dweight)
+        return copy_rows(dweight, sizeof(float) * lddw, dw, sizeof(float) * p->d, sizeof(float) * p->d, p->v, stream);
     return FCE_OK;
 }
 

@@ -55,7 +55,8 @@ def lce_backward(hidden: torch.Tensor, weight: torch.Tensor, targets: torch.Tens
     if reduction == 2:
         upstream = grad_out.float().contiguous()
     else:
-        upstream = float(grad_out.item())
+        # read on the device (fce_backward_dev): no host sync, CUDA-graph capturable
+        upstream = grad_out.float().reshape(())
     # gradients come out of the library in the parameters' dtype (bf16 dW is
     # rounded straight from the tensor-core accumulators)
     gdt = torch.bfloat16 if weight.dtype == torch.bfloat16 else torch.float32

@@ -2,10 +2,14 @@
 
 Two front ends over the same per-rank CUDA work:
 
-* ``NativeComm`` / ``native_forward`` / ``native_backward`` drive the C-ABI in
-  ``include/fce/fce_vp.h``: NCCL is owned by libfce.so and the collectives run
-  on the handle's stream (what a C++ caller of the drop-in ``tp_forward`` /
-  ``tp_backward`` gets).
+* ``NativeComm`` / ``native_forward`` / ``native_backward`` /
+  ``native_sp_gather`` / ``native_sp_scatter`` / ``native_dp_step`` drive the
+  C-ABI in ``include/fce/fce_vp.h``: the communicator is owned by libfce.so
+  (NCCL, one process per GPU; or ``LocalGroup``: k ranks as k threads of one
+  process, collectives by libfce's peer-memory kernels — ``run_ranks`` runs a
+  k-rank job that way on one GPU) and the collectives run on the handle's
+  stream (what a C++ caller of the drop-in ``tp_forward`` / ``tp_backward``
+  gets).
 * ``VocabParallel`` does the same exchange with ``torch.distributed``
   collectives, with the per-rank compute injectable.  On GPUs the compute is
   the CUDA path (``CudaCompute``); the gloo tests plug the CPU oracle in to
@@ -52,7 +56,15 @@ class NativeComm:
 
     @classmethod
     def create_local(cls, device: int = 0) -> "NativeComm":
+        """A 1-rank NCCL communicator on `device`."""
         return cls.create(1, 0, device, cls.unique_id())
+
+    def query(self):
+        """(nranks, rank, transport) with transport 1 = NCCL, 2 = local."""
+        lib = fce.load_library()
+        k, r, t = ctypes.c_int(), ctypes.c_int(), ctypes.c_int()
+        fce._check(lib.fce_comm_query(self.ptr, ctypes.byref(k), ctypes.byref(r), ctypes.byref(t)), vp=True)
+        return k.value, r.value, t.value
 
     @classmethod
     def from_torch_distributed(cls, device: int, group=None) -> "NativeComm":
@@ -67,6 +79,81 @@ class NativeComm:
         if self.ptr:
             fce.load_library().fce_comm_destroy(self.ptr)
             self.ptr = None
+
+
+class LocalGroup:
+    """In-process communicator group (fce_comm_group_create): `nranks` ranks of
+    this process, each driven by its own host thread, on any devices (several
+    may share one GPU).  Its collectives are libfce's own peer-memory kernels,
+    so the k-rank vocab-parallel / SP / DP code runs on a single B200."""
+
+    def __init__(self, nranks: int):
+        lib = fce.load_library()
+        self.nranks = nranks
+        self.ptr = ctypes.c_void_p()
+        fce._check(lib.fce_comm_group_create(ctypes.byref(self.ptr), nranks), vp=True)
+
+    def comm(self, rank: int, device: int = 0) -> NativeComm:
+        lib = fce.load_library()
+        ptr = ctypes.c_void_p()
+        fce._check(lib.fce_comm_init_local(ctypes.byref(ptr), self.ptr, device, rank), vp=True)
+        return NativeComm(ptr, self.nranks, rank, device)
+
+    def close(self):
+        if self.ptr:
+            fce.load_library().fce_comm_group_destroy(self.ptr)
+            self.ptr = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def run_ranks(nranks: int, fn, devices=None):
+    """Run ``fn(rank, comm, handle)`` for every rank of a fresh LocalGroup, each
+    on its own host thread, CUDA stream and library handle (what one process
+    per GPU gives each rank).  Returns the per-rank results in rank order and
+    re-raises the first rank's exception.  ctypes releases the GIL inside the
+    library, so the ranks meet in the collectives concurrently."""
+    import threading
+
+    import torch
+    devices = devices or [0] * nranks
+    for d in set(devices):
+        torch.cuda.synchronize(d)  # inputs made on the default stream are ready
+    group = LocalGroup(nranks)
+    comms = [group.comm(r, devices[r]) for r in range(nranks)]
+    results = [None] * nranks
+    errors = [None] * nranks
+
+    def body(r):
+        try:
+            torch.cuda.set_device(devices[r])
+            stream = torch.cuda.Stream(devices[r])
+            with torch.cuda.stream(stream):
+                h = fce.Handle(devices[r], stream)
+                try:
+                    results[r] = fn(r, comms[r], h)
+                    stream.synchronize()
+                finally:
+                    h.close()
+        except BaseException as exc:  # noqa: BLE001 - handed to the caller
+            errors[r] = exc
+
+    threads = [threading.Thread(target=body, args=(r,), name=f"fce-rank{r}") for r in range(nranks)]
+    for t in threads:
+        t.start()
+    for t in threads:
+        t.join()
+    for c in comms:
+        c.close()
+    group.close()
+    for e in errors:
+        if e is not None:
+            raise e
+    return results
 
 
 def native_forward(comm: NativeComm, hidden, weight_shard, targets, v_offset: int, v_total: int,
@@ -87,20 +174,99 @@ def native_forward(comm: NativeComm, hidden, weight_shard, targets, v_offset: in
 
 def native_backward(comm: NativeComm, hidden, weight_shard, targets, v_offset: int, v_total: int,
                     stats: fce.Stats, reduction: str = "mean", upstream=1.0, ignore_index=None,
-                    handle=None):
-    """tp_backward over real ranks (fce_vp_backward) -> (dH summed over ranks, local dW shard)."""
+                    handle=None, dhidden=None):
+    """tp_backward over real ranks (fce_vp_backward) -> (dH summed over ranks, local dW shard).
+    `dhidden` may be a caller-owned fp32 [N, >= d] view (any row stride)."""
     import torch
     h = handle or fce.default_handle(hidden.device.index or 0)
     p, keep = fce.make_problem(hidden, weight_shard, targets, ignore_index, v_offset, v_total)
     dev = hidden.device
-    dh = torch.empty(p.n, p.d, dtype=torch.float32, device=dev)
+    dh = dhidden if dhidden is not None else torch.empty(p.n, p.d, dtype=torch.float32, device=dev)
     dw = torch.empty(p.v, p.d, dtype=torch.float32, device=dev)
     up_rows = None if isinstance(upstream, (int, float)) else upstream.float().contiguous()
+    if up_rows is not None and up_rows.numel() != p.n:
+        raise fce.InconsistentUpstream(f"per-position upstream has {up_rows.numel()} entries, expected {p.n}")
     fce._check(h.lib.fce_vp_backward(h.raw, comm.ptr, ctypes.byref(p), stats.c(),
                                      fce.REDUCTIONS[reduction],
                                      float(upstream) if up_rows is None else 0.0,
-                                     fce._ptr(up_rows), dh.data_ptr(), p.d, dw.data_ptr(), p.d))
+                                     fce._ptr(up_rows), dh.data_ptr(), dh.stride(0), dw.data_ptr(), p.d))
     return dh, dw
+
+
+def native_sp_gather(comm: NativeComm, hidden_shard, n_total: int, handle=None):
+    """sp_to_tp_gather (parallel_sim.hpp:294-314) through fce_sp_gather: this
+    rank's position shard of H (bf16) -> the full H on every rank."""
+    import torch
+    h = handle or fce.default_handle(hidden_shard.device.index or 0)
+    x = fce._as_operand(hidden_shard, "hidden") if hidden_shard.shape[0] else hidden_shard
+    d = hidden_shard.shape[1]
+    ld = (d + 7) // 8 * 8
+    full = torch.empty(n_total, ld, dtype=torch.bfloat16, device=hidden_shard.device)[:, :d]
+    fce._check(h.lib.fce_sp_gather(h.raw, comm.ptr, x.data_ptr() if x.shape[0] else None, x.shape[0],
+                                   x.stride(0) if x.shape[0] else d, d, n_total, full.data_ptr(),
+                                   full.stride(0)), vp=True)
+    return full
+
+
+def native_sp_scatter(comm: NativeComm, dh_partial, shard_rows: int, handle=None):
+    """Reduce-scatter of full-length dH partials to this rank's position shard (fce_sp_scatter)."""
+    import torch
+    h = handle or fce.default_handle(dh_partial.device.index or 0)
+    dh_partial = dh_partial.float()
+    if dh_partial.stride(1) != 1:
+        dh_partial = dh_partial.contiguous()
+    n, d = dh_partial.shape
+    out = torch.empty(shard_rows, d, dtype=torch.float32, device=dh_partial.device)
+    fce._check(h.lib.fce_sp_scatter(h.raw, comm.ptr, dh_partial.data_ptr(), n, dh_partial.stride(0), d,
+                                    out.data_ptr() if shard_rows else None, shard_rows, d), vp=True)
+    return out
+
+
+def native_dp_step(comm: NativeComm, hidden, weight, targets, reduction="mean", ignore_index=None,
+                   want_dhidden=True, handle=None):
+    """dp_step (parallel_sim.hpp:334-378) through fce_dp_step -> (loss averaged
+    over replicas, local dH or None, dW averaged over replicas)."""
+    import torch
+    h = handle or fce.default_handle(hidden.device.index or 0)
+    if reduction not in fce.REDUCTIONS:
+        raise fce.UnsupportedReduction(reduction)
+    p, keep = fce.make_problem(hidden, weight, targets, ignore_index)
+    dev = hidden.device
+    loss = torch.empty((), dtype=torch.float32, device=dev)
+    dh = torch.empty(p.n, p.d, dtype=torch.float32, device=dev) if want_dhidden else None
+    dw = torch.empty(p.v, p.d, dtype=torch.float32, device=dev)
+    fce._check(h.lib.fce_dp_step(h.raw, comm.ptr, ctypes.byref(p), fce.REDUCTIONS[reduction], loss.data_ptr(),
+                                 fce._ptr(dh), p.d, dw.data_ptr(), p.d), vp=True)
+    return loss, dh, dw
+
+
+def native_all_reduce(comm: NativeComm, x, handle=None):
+    """In-place fp32 sum over the ranks (fce_comm_all_reduce_f32)."""
+    h = handle or fce.default_handle(x.device.index or 0)
+    fce._check(h.lib.fce_comm_all_reduce_f32(h.raw, comm.ptr, x.data_ptr(), x.data_ptr(), x.numel()), vp=True)
+    return x
+
+
+def native_all_gather(comm: NativeComm, x, handle=None):
+    """[nranks, *x.shape] of every rank's x (fce_comm_all_gather)."""
+    import torch
+    h = handle or fce.default_handle(x.device.index or 0)
+    x = x.contiguous()
+    out = torch.empty((comm.nranks,) + tuple(x.shape), dtype=x.dtype, device=x.device)
+    fce._check(h.lib.fce_comm_all_gather(h.raw, comm.ptr, x.data_ptr(), out.data_ptr(),
+                                         x.numel() * x.element_size()), vp=True)
+    return out
+
+
+def native_reduce_scatter(comm: NativeComm, x, handle=None):
+    """x: fp32 [nranks * m] -> this rank's [m] block of the sum over ranks."""
+    import torch
+    h = handle or fce.default_handle(x.device.index or 0)
+    x = x.float().contiguous()
+    m = x.numel() // comm.nranks
+    out = torch.empty(m, dtype=torch.float32, device=x.device)
+    fce._check(h.lib.fce_comm_reduce_scatter_f32(h.raw, comm.ptr, x.data_ptr(), out.data_ptr(), m), vp=True)
+    return out
 
 
 # ------------------------------------------------------- torch.distributed

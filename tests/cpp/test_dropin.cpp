@@ -218,6 +218,21 @@ static void test_sp_dp() {
     CHECK(ledger.current_bytes() == 0);
 }
 
+static void test_forward_memory_is_v_independent() {
+    // test_fused_forward.cpp:217-232: the forward's auxiliary memory is
+    // 2 N sizeof(SoftmaxStats) + N sizeof(T), whatever V is
+    const std::size_t n = 16, d = 8;
+    const std::size_t expect = 2 * n * sizeof(SoftmaxStats<float>) + n * sizeof(float);
+    for (std::size_t v : {64, 512, 2048}) {
+        Instance<float> inst = instance(n, d, v, 13, 0.0);
+        MemoryLedger ledger;
+        (void)fused_forward(MatrixView<float>(inst.hidden), MatrixView<float>(inst.weights), inst.targets,
+                            ReductionMode::Mean, ledger);
+        CHECK(ledger.peak_bytes() == expect);
+        CHECK(ledger.current_bytes() == 0);
+    }
+}
+
 int main() {
     std::printf("drop-in C++ API tests\n");
     test_worked_example();
@@ -228,6 +243,7 @@ int main() {
     test_errors();
     test_tp_matches_single();
     test_sp_dp();
+    test_forward_memory_is_v_independent();
     std::printf("%d checks, %d failed\n", g_checks, g_fail);
     return g_fail ? 1 : 0;
 }

@@ -55,7 +55,7 @@ def test_gpu_arm_native_vocab_parallel_under_torchrun(cuda):
     assert len(lines) == 1
     d = lines[0]
     assert BASE_KEYS <= set(d) and {"roofline", "clocks", "gpu_launches"} <= set(d)
-    assert d["config"]["parallelism"] == "vocab-parallel x1"
+    assert d["config"]["parallelism"].startswith("vocab-parallel x1 (NCCL")
     assert d["gpu_launches"] > 0 and d["value"] > 0 and d["e2e"]["h2d_bytes_per_step"] > 0
     # same loss as the single-GPU path on the same seeded instance
     r1 = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--config", "small", "--steps", "2",
@@ -64,3 +64,33 @@ def test_gpu_arm_native_vocab_parallel_under_torchrun(cuda):
     assert r1.returncode == 0, r1.stderr[-3000:]
     d1 = _json_lines(r1.stdout)[0]
     assert abs(d["loss"] - d1["loss"]) <= 1e-6 * abs(d1["loss"])
+
+
+@pytest.mark.gpu
+def test_gpu_arm_self_launches_k_ranks_without_torchrun(cuda):
+    """`bench.py --gpus 3` launched plainly on a box with fewer GPUs runs the 3
+    ranks of the vocab-parallel path in-process (local transport) and prints
+    one JSON line whose loss equals the single-GPU path's."""
+    r = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--gpus", "3", "--config", "small",
+                        "--steps", "2", "--warmup", "3", "--e2e-steps", "2", "--no-cpu-baseline"], cwd=ROOT,
+                       capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stderr[-3000:]
+    lines = _json_lines(r.stdout)
+    assert len(lines) == 1
+    d = lines[0]
+    assert BASE_KEYS <= set(d) and d["config"]["ranks"] == 3
+    assert "local transport" in d["config"]["parallelism"]
+    assert d["e2e_with_grads"]["d2h_bytes_per_step"] > d["e2e"]["d2h_bytes_per_step"]
+    r1 = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--config", "small", "--steps", "2",
+                         "--warmup", "3", "--e2e-steps", "2", "--no-cpu-baseline"], cwd=ROOT, capture_output=True,
+                        text=True, timeout=600)
+    assert r1.returncode == 0, r1.stderr[-3000:]
+    d1 = _json_lines(r1.stdout)[0]
+    assert abs(d["loss"] - d1["loss"]) <= 1e-5 * abs(d1["loss"])
+
+
+def test_cpu_baseline_fit_is_the_marginal_cost():
+    sys.path.insert(0, ROOT)
+    import bench
+    alpha, beta = bench._fit([(16, 10.0), (208, 14.8), (16, 10.2), (208, 15.0)])
+    assert abs(beta - 0.025) < 1e-9 and abs(alpha - (10.1 - 0.025 * 16)) < 1e-9

@@ -1,0 +1,259 @@
+"""Multi-rank C-ABI (include/fce/fce_vp.h) with k > 1 real ranks on one B200.
+
+The ranks are k host threads of this process, each with its own CUDA stream,
+library handle and communicator of one in-process group (the "local"
+transport: libfce's own peer-memory collectives).  Every rank runs exactly the
+code a one-process-per-GPU NCCL job runs — fce_vp_forward / fce_vp_backward /
+fce_sp_gather / fce_sp_scatter / fce_dp_step — and the results are checked
+against the CPU oracle's restatement of the reference's tp_forward /
+tp_backward / sp_to_tp_gather / dp_step (parallel_sim.hpp:165-378) on the same
+bf16-grid inputs.  Tolerances as tests/test_parity_gpu.py: loss / lse 1e-3
+relative, dH / dW 1e-2 relative max-norm, found flags and ignored rows exact.
+"""
+import numpy as np
+import pytest
+import torch
+
+import paper_2511_17599_b200 as fce
+from paper_2511_17599_b200 import vocab_parallel as vp
+from oracle import bindings as ob
+
+pytestmark = pytest.mark.gpu
+
+LOSS_RTOL = 1e-3
+GRAD_RTOL = 1e-2
+
+
+def relmax(got, ref):
+    got = np.asarray(got, np.float64)
+    ref = np.asarray(ref, np.float64)
+    scale = np.abs(ref).max()
+    return float(np.abs(got - ref).max() / scale) if scale else float(np.abs(got).max())
+
+
+def bf16(x):
+    return torch.from_numpy(np.ascontiguousarray(x)).cuda().to(torch.bfloat16)
+
+
+def vp_step(k, H, W, Y, ign, reduction, upstream=1.0, strided_dh=False):
+    """k-rank tp_forward + tp_backward; returns per-rank (out, dH, dW shard)."""
+    n, d = H.shape
+    v = W.shape[0]
+    Hd, Wd, Yd = bf16(H), bf16(W), torch.from_numpy(Y).cuda()
+    up = upstream if np.isscalar(upstream) else torch.from_numpy(np.asarray(upstream, np.float32)).cuda()
+    ranges = fce.shard_ranges(v, k)
+
+    def rank_fn(r, comm, h):
+        lo, hi = ranges[r]
+        out = vp.native_forward(comm, Hd, Wd[lo:hi], Yd, lo, v, reduction, ign, handle=h)
+        dh_buf = None
+        if strided_dh:
+            dh_buf = torch.full((n, d + 12), 7.0, dtype=torch.float32, device="cuda")[:, :d]
+        dh, dw = vp.native_backward(comm, Hd, Wd[lo:hi], Yd, lo, v, out.stats, reduction, up, ign,
+                                    handle=h, dhidden=dh_buf)
+        if strided_dh:
+            # columns past d belong to the caller: untouched
+            assert torch.all(dh_buf.as_strided((n, 12), (d + 12, 1), d) == 7.0)
+        return out, dh, dw
+
+    return vp.run_ranks(k, rank_fn)
+
+
+@pytest.mark.parametrize("k,reduction,ign,frac,strided", [
+    (2, "sum", None, 0.0, True),
+    (3, "mean", -100, 0.25, False),
+    (8, "none", -1, 0.2, False),
+    (5, "mean", None, 0.0, False),
+])
+def test_vocab_parallel_k_ranks_match_oracle(cuda, k, reduction, ign, frac, strided):
+    n, d, v = 200, 136, 1500
+    H, W, Y = ob.make_instance(n, d, v, 11 + k, -100 if ign is None else ign, frac)
+    rng = np.random.default_rng(k)
+    upstream = rng.standard_normal(n).astype(np.float32) if reduction == "none" else 1.0
+    res = vp_step(k, H, W, Y, ign, reduction, upstream, strided)
+    st, rows, lred = ob.forward(H, W, Y, reduction, ign)
+    dH, dW = ob.backward(H, W, Y, st, reduction, upstream, ign)
+    valid = np.ones(n, bool) if ign is None else Y != ign
+    lse_ref = st["m"] + np.log(np.where(valid, st["a"], 1))
+    out0 = res[0][0]
+    for r, (out, dh, dw) in enumerate(res):
+        # every rank holds the same merged stats / loss (rank-ordered merge)
+        np.testing.assert_array_equal(out.stats.found.cpu().numpy(), st["found"])
+        np.testing.assert_array_equal(out.stats.m.cpu().numpy(), out0.stats.m.cpu().numpy())
+        np.testing.assert_array_equal(out.loss_rows.cpu().numpy(), out0.loss_rows.cpu().numpy())
+        lse = out.lse.cpu().numpy()
+        assert np.max(np.abs(lse[valid] - lse_ref[valid]) / np.maximum(1, np.abs(lse_ref[valid]))) < LOSS_RTOL
+        got_rows = out.loss_rows.cpu().numpy()
+        assert np.all(got_rows[~valid] == 0.0)
+        assert np.max(np.abs(got_rows - rows) / np.maximum(1, np.abs(rows))) < LOSS_RTOL
+        if reduction != "none":
+            assert abs(out.loss.item() - lred) <= LOSS_RTOL * max(1.0, abs(lred))
+        # dH: the all-reduced sum over the k shards, identical on every rank
+        dh_np = dh.cpu().numpy()
+        assert relmax(dh_np, dH) < GRAD_RTOL, (r, relmax(dh_np, dH))
+        np.testing.assert_array_equal(dh_np, res[0][1].cpu().numpy())
+        if ign is not None:
+            assert np.all(dh_np[~valid] == 0.0)
+    # dW stays sharded: the concatenation of the rank shards is the full dW
+    dw_all = np.concatenate([x[2].cpu().numpy() for x in res])
+    assert dw_all.shape == dW.shape
+    assert relmax(dw_all, dW) < GRAD_RTOL
+
+
+def test_vocab_parallel_matches_single_rank_path(cuda):
+    n, d, v = 256, 264, 2048
+    H, W, Y = ob.make_instance(n, d, v, 3, -100, 0.1)
+    res = vp_step(4, H, W, Y, -100, "mean")
+    Hd, Wd, Yd = bf16(H), bf16(W), torch.from_numpy(Y).cuda()
+    one = fce.fused_forward(Hd, Wd, Yd, "mean", -100)
+    dh1, dw1 = fce.fused_backward_recompute(Hd, Wd, Yd, one.stats, "mean", 1.0, -100)
+    out, dh, _ = res[0]
+    np.testing.assert_array_equal(out.stats.found.cpu().numpy(), one.stats.found.cpu().numpy())
+    assert abs(out.loss.item() - one.loss.item()) <= 1e-5 * abs(one.loss.item())
+    assert relmax(dh.cpu().numpy(), dh1.cpu().numpy()) < 1e-3
+    dw_all = torch.cat([x[2] for x in res]).cpu().numpy()
+    assert relmax(dw_all, dw1.cpu().numpy()) < 1e-3
+
+
+def test_vocab_parallel_target_errors_raise_on_every_rank(cuda):
+    n, d, v = 64, 72, 600
+    H, W, Y = ob.make_instance(n, d, v, 5)
+    Y = Y.copy()
+    Y[7] = v + 3  # outside [0, V): every rank's validation rejects it before any collective
+    Hd, Wd, Yd = bf16(H), bf16(W), torch.from_numpy(Y).cuda()
+    ranges = fce.shard_ranges(v, 3)
+    caught = []
+
+    def rank_fn(r, comm, h):
+        lo, hi = ranges[r]
+        try:
+            vp.native_forward(comm, Hd, Wd[lo:hi], Yd, lo, v, "mean", None, handle=h)
+        except fce.TargetOutOfRange:
+            caught.append(r)
+
+    vp.run_ranks(3, rank_fn)
+    assert sorted(caught) == [0, 1, 2]
+
+
+def test_comm_query_and_collectives_are_rank_ordered(cuda):
+    k = 5
+    rng = np.random.default_rng(0)
+    xs = [rng.standard_normal(1003).astype(np.float32) * 10 ** r for r in range(k)]
+    ref = xs[0].copy()
+    for x in xs[1:]:
+        ref = (ref + x).astype(np.float32)  # sequential fp32 adds in rank order
+
+    def rank_fn(r, comm, h):
+        assert comm.query() == (k, r, 2)
+        x = torch.from_numpy(xs[r]).cuda()
+        s = vp.native_all_reduce(comm, x.clone(), handle=h)
+        g = vp.native_all_gather(comm, torch.full((3,), float(r), device="cuda"), handle=h)
+        big = torch.arange(k * 7, dtype=torch.float32, device="cuda") * (r + 1)
+        rs = vp.native_reduce_scatter(comm, big, handle=h)
+        return s.cpu().numpy(), g.cpu().numpy(), rs.cpu().numpy()
+
+    res = vp.run_ranks(k, rank_fn)
+    tot = sum(range(1, k + 1))
+    for r, (s, g, rs) in enumerate(res):
+        np.testing.assert_array_equal(s, ref)  # bit-exact: the local transport sums in rank order
+        np.testing.assert_array_equal(g, np.repeat(np.arange(k, dtype=np.float32)[:, None], 3, 1))
+        np.testing.assert_array_equal(rs, np.arange(r * 7, r * 7 + 7, dtype=np.float32) * tot)
+
+
+@pytest.mark.parametrize("k,sizes", [(3, None), (4, [5, 0, 40, 19])])
+def test_sp_gather_and_scatter(cuda, k, sizes):
+    n, d = 64, 40
+    rng = np.random.default_rng(k)
+    H = ob.make_instance(n, d, 10, 1)[0]
+    if sizes is None:
+        ranges = fce.shard_ranges(n, k)
+    else:
+        edges = np.concatenate([[0], np.cumsum(sizes)])
+        ranges = [(int(edges[i]), int(edges[i + 1])) for i in range(k)]
+    parts = [rng.standard_normal((n, d)).astype(np.float32) for _ in range(k)]
+    Hd = bf16(H)
+
+    def rank_fn(r, comm, h):
+        lo, hi = ranges[r]
+        full = vp.native_sp_gather(comm, Hd[lo:hi], n, handle=h)
+        shard = vp.native_sp_scatter(comm, torch.from_numpy(parts[r]).cuda(), hi - lo, handle=h)
+        return full.float().cpu().numpy(), shard.cpu().numpy()
+
+    res = vp.run_ranks(k, rank_fn)
+    total = parts[0].copy()
+    for p_ in parts[1:]:
+        total = (total + p_).astype(np.float32)
+    for r, (full, shard) in enumerate(res):
+        np.testing.assert_array_equal(full, H)  # bf16-grid H gathers exactly, in position order
+        lo, hi = ranges[r]
+        np.testing.assert_array_equal(shard, total[lo:hi])
+
+
+def test_sp_gather_rejects_bad_layouts(cuda):
+    n, d = 30, 16
+    H = bf16(ob.make_instance(n, d, 10, 1)[0])
+    errs = {}
+
+    def rank_fn(r, comm, h):
+        try:  # rows do not add up to n
+            vp.native_sp_gather(comm, H[:10], n + 5, handle=h)
+        except fce.DimensionMismatch:
+            errs.setdefault("rows", []).append(r)
+        try:  # widths disagree (sp_to_tp_gather: "hidden shards disagree on width")
+            vp.native_sp_gather(comm, H[:15, : 8 + 8 * r], n, handle=h)
+        except fce.InvalidLayout:
+            errs.setdefault("width", []).append(r)
+
+    vp.run_ranks(2, rank_fn)
+    assert sorted(errs["rows"]) == [0, 1] and sorted(errs["width"]) == [0, 1]
+
+
+@pytest.mark.parametrize("k,reduction", [(2, "mean"), (3, "sum")])
+def test_dp_step_matches_oracle(cuda, k, reduction):
+    n, d, v = 96, 104, 900
+    W = ob.make_instance(n, d, v, 100)[1]
+    reps = [ob.make_instance(n, d, v, 200 + r, -100, 0.2) for r in range(k)]
+    Wd = bf16(W)
+
+    def rank_fn(r, comm, h):
+        H, _, Y = reps[r]
+        loss, dh, dw = vp.native_dp_step(comm, bf16(H), Wd, torch.from_numpy(Y).cuda(), reduction, -100, handle=h)
+        return loss.item(), dh.cpu().numpy(), dw.cpu().numpy()
+
+    res = vp.run_ranks(k, rank_fn)
+    losses, dws, dhs = [], [], []
+    for r in range(k):
+        H, _, Y = reps[r]
+        st, _, lred = ob.forward(H, W, Y, reduction, -100)
+        dH, dW_ = ob.backward(H, W, Y, st, reduction, 1.0, -100)
+        losses.append(lred)
+        dws.append(dW_)
+        dhs.append(dH)
+    loss_ref = sum(losses) / k
+    dw_ref = sum(dws) / k
+    for r, (loss, dh, dw) in enumerate(res):
+        assert abs(loss - loss_ref) <= LOSS_RTOL * max(1.0, abs(loss_ref))
+        assert relmax(dw, dw_ref) < GRAD_RTOL
+        assert relmax(dh, dhs[r]) < GRAD_RTOL  # dH stays rank-local
+        np.testing.assert_array_equal(dw, res[0][2])
+
+
+def test_dp_step_rejects_unequal_micro_batches_and_none(cuda):
+    d, v = 40, 300
+    W = bf16(ob.make_instance(4, d, v, 1)[1])
+    got = {}
+
+    def rank_fn(r, comm, h):
+        n = 32 + 16 * r
+        H, _, Y = ob.make_instance(n, d, v, r)
+        try:
+            vp.native_dp_step(comm, bf16(H), W, torch.from_numpy(Y).cuda(), "mean", handle=h)
+        except fce.InvalidLayout:
+            got.setdefault("sizes", []).append(r)
+        try:
+            vp.native_dp_step(comm, bf16(H), W, torch.from_numpy(Y).cuda(), "none", handle=h)
+        except fce.UnsupportedReduction:
+            got.setdefault("none", []).append(r)
+
+    vp.run_ranks(2, rank_fn)
+    assert sorted(got["sizes"]) == [0, 1] and sorted(got["none"]) == [0, 1]

@@ -701,9 +701,35 @@ def test_full_size_configs(cuda, name, n, d, v, frac):
     # sum_v G[n, v] = 0 per row => dW columns sum to ~0 (test_reference.cpp:218-233)
     col = dw.double().sum(0)
     assert col.abs().max().item() < 1e-3 * dw.abs().max().item() * math.sqrt(v)
+    # dW rows against the oracle: every row of dW contracts all N rows of G and
+    # H, so vocab slices in the first band, the middle, the last (partial) band
+    # and the last tile check the band / row-chunk geometry of the default plan
+    # (fused_backward.hpp:47-52; two row chunks at Llama-3-70B)
+    check_dw_slices(Hd, Wd, Yd, out.stats, dw, ign, v)
     # linearity: upstream 2 doubles both gradients exactly
     dh2, dw2 = fce.fused_backward_recompute(Hd, Wd, Yd, out.stats, "sum", 2.0, ign)
     assert torch.equal(dh2, 2 * dh) and torch.equal(dw2, 2 * dw)
+
+
+def check_dw_slices(Hd, Wd, Yd, stats, dw, ign, v, band=3072, width=8):
+    """dW[v0:v0+width] of a full-size sum-reduction backward vs the oracle run
+    on that vocabulary slice (v_offset / v_total set) over all N rows with the
+    device's forward stats."""
+    Hn = Hd.float().cpu().numpy()
+    Yn = Yd.cpu().numpy()
+    n = Hn.shape[0]
+    st = np.zeros(n, ob.STATS_DTYPE)
+    st["m"] = stats.m.cpu().numpy()
+    st["a"] = stats.a.cpu().numpy()
+    st["z_target"] = stats.z_target.cpu().numpy()
+    st["found"] = stats.found.cpu().numpy()
+    last_band = band * ((v - 1) // band)
+    starts = sorted({0, v // 2 - width // 2, last_band, v - width})
+    for v0 in starts:
+        Ws = Wd[v0:v0 + width].float().cpu().numpy()
+        _, dW_ref = ob.backward(Hn, Ws, Yn, st, "sum", 1.0, ign, v_offset=v0, want_dh=False, v_total=v)
+        err = relmax(dw[v0:v0 + width].cpu().numpy(), dW_ref)
+        assert err < GRAD_RTOL, (v0, err)
 
 
 @pytest.mark.slow

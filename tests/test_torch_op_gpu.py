@@ -1,4 +1,5 @@
 """The PyTorch autograd op over the C-ABI against a plain PyTorch fp32 reference."""
+import numpy as np
 import pytest
 import torch
 
@@ -97,3 +98,49 @@ def test_loss_module_with_batch_dims(cuda):
     assert hidden.grad.shape == (B, T, D)
     per_tok = FusedLinearCrossEntropyLoss("none")(hidden.detach(), head.weight.detach(), targets)
     assert per_tok.shape == (B, T) and torch.all(per_tok[:, :10] == 0)
+
+
+def test_autograd_step_is_cuda_graph_capturable(cuda):
+    """loss.backward() through the custom op inside torch.cuda.graph: the scalar
+    upstream is read on the device (fce_backward_dev), so with validation off
+    the whole autograd step is stream-ordered and replays with new inputs."""
+    import paper_2511_17599_b200 as fce
+    from oracle import bindings as ob
+    n, d, v = 192, 136, 1500
+    H, W, Y = ob.make_instance(n, d, v, 21, -100, 0.2)
+    h = fce.default_handle(0)
+    h.set_option("validate", 0)
+    try:
+        hid = torch.from_numpy(H).cuda().to(torch.bfloat16).requires_grad_()
+        w = torch.from_numpy(W).cuda().to(torch.bfloat16).requires_grad_()
+        y = torch.from_numpy(Y).cuda()
+        s = torch.cuda.Stream()
+        s.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(s):  # warm-up on the capture stream (allocator, workspaces)
+            for _ in range(2):
+                hid.grad = w.grad = None
+                loss = fused_linear_cross_entropy(hid, w, y, "mean", -100)
+                loss.backward()
+        torch.cuda.current_stream().wait_stream(s)
+        g = torch.cuda.CUDAGraph()
+        hid.grad = w.grad = None
+        with torch.cuda.graph(g):
+            loss = fused_linear_cross_entropy(hid, w, y, "mean", -100)
+            loss.backward()
+        # new inputs in place, replay, compare with the oracle
+        H2, W2, Y2 = ob.make_instance(n, d, v, 22, -100, 0.2)
+        with torch.no_grad():
+            hid.copy_(torch.from_numpy(H2).cuda().to(torch.bfloat16))
+            w.copy_(torch.from_numpy(W2).cuda().to(torch.bfloat16))
+            y.copy_(torch.from_numpy(Y2).cuda())
+        g.replay()
+        torch.cuda.synchronize()
+        st, _, lred = ob.forward(H2, W2, Y2, "mean", -100)
+        dH, dW = ob.backward(H2, W2, Y2, st, "mean", 1.0, -100)
+        assert abs(loss.item() - lred) <= 1e-3 * abs(lred)
+        gh = hid.grad.float().cpu().numpy()
+        gw = w.grad.float().cpu().numpy()
+        assert np.abs(gh - dH).max() / np.abs(dH).max() < 2e-2
+        assert np.abs(gw - dW).max() / np.abs(dW).max() < 2e-2
+    finally:
+        h.set_option("validate", 1)
