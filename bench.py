@@ -553,7 +553,7 @@ def bench_rank(ctx, args):
 def _traffic_from_profile(cfg, kernel):
     """DRAM bytes per launch of the dominant kernel from the committed ncu
     capture of the CURRENT kernel sources (profiles/traffic.json records the
-    hash of csrc/*.cu|*.cuh|*.h it was captured on; a stale entry is not
+    hash of csrc/*.cu|*.cuh it was captured on; a stale entry is not
     reported)."""
     tpath = os.path.join(ROOT, "profiles", "traffic.json")
     if not os.path.exists(tpath):
@@ -576,7 +576,7 @@ def _source_hash():
     hsh = hashlib.sha256()
     csrc = os.path.join(ROOT, "paper_2511_17599_b200", "csrc")
     for name in sorted(os.listdir(csrc)):
-        if name.endswith((".cu", ".cuh", ".h")):
+        if name.endswith((".cu", ".cuh")):
             with open(os.path.join(csrc, name), "rb") as f:
                 hsh.update(f.read())
     return hsh.hexdigest()[:16]

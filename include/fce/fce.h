@@ -96,7 +96,13 @@ const char* fce_status_string(fce_status s);
  * "band_cols" / "row_chunk" (backward G chunk, 0 = auto), "bwd_persistent"
  * (1 = one persistent backward launch, default; 0 = two launches per chunk), "validate"
  * (1 = sync and check targets / stats, default 1), "timing" (1 = per-kernel
- * event timing, see fce_kernel_stats; setting it resets the counters). */
+ * event timing, see fce_kernel_stats; setting it resets the counters),
+ * "skip_ignored" (1 = compact ignored rows away before the tile kernels,
+ * default), "bwd_reserve_sms" (SMs the persistent backward leaves free),
+ * "vp_overlap_chunks" (fce_vp_backward: 0 = one dH all-reduce after the
+ * kernel, default; k >= 2 = rows in k chunks, each chunk's all-reduce
+ * released by the kernel's completion counter and overlapped with the later
+ * chunks) and "vp_reserve_sms" (SMs left to those collectives, default 8). */
 fce_status fce_set_option(fce_handle h, const char* key, int64_t value);
 /* Library-owned device workspace (the device analogue of MemoryLedger,
  * memory_ledger.hpp:18-62): bytes held now and the high-water mark. */

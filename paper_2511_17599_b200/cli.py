@@ -11,7 +11,8 @@ latency_min_s,latency_max_s,aux_peak_bytes,loss — `canonical` is the two-stage
 PyTorch path (cuBLAS lm_head GEMM + cross-entropy, materialises N x V logits).
 `verify` checks the fused device path against that two-stage path in fp32 on
 random instances (loss equivalence, gradients, window sweep, shard invariance,
-large-offset stability) and prints one line per suite.  Exit codes follow the
+large-offset stability, k-rank vocab-parallel over the in-process transport
+against the one-rank path) and prints one line per suite.  Exit codes follow the
 reference CLI: 0 pass, 1 tolerance failure, 2 usage / library error.
 """
 from __future__ import annotations
@@ -178,12 +179,37 @@ def cmd_verify(a) -> int:
         return float("inf") if not torch.isfinite(got).all() else rel(got, ref)
     stability.count = 3
 
+    def vocab_parallel(i):
+        # tp_forward / tp_backward over k real ranks (in-process local transport:
+        # k threads, each with its own stream / handle / communicator) against
+        # the one-rank path (verify.cpp shard-invariance suite, parallel_sim.hpp)
+        from paper_2511_17599_b200 import vocab_parallel as vp
+        k = 2 + i
+        n, d, v = 96, 72, 777
+        H, W, Y = fce.generate_instance(n, d, v, a.seed + 31 + i, -100, 0.2)
+        one = fce.fused_forward(H, W, Y, "mean", -100)
+        dh1, dw1 = fce.fused_backward_recompute(H, W, Y, one.stats, "mean", 1.0, -100)
+        ranges = fce.shard_ranges(v, k)
+
+        def rank_fn(r, comm, hh):
+            lo, hi = ranges[r]
+            out = vp.native_forward(comm, H, W[lo:hi], Y, lo, v, "mean", -100, handle=hh)
+            dh, dw = vp.native_backward(comm, H, W[lo:hi], Y, lo, v, out.stats, "mean", 1.0, -100, handle=hh)
+            return out.loss, dh, dw
+
+        res = vp.run_ranks(k, rank_fn)
+        err = abs(res[0][0].item() - one.loss.item()) / abs(one.loss.item())
+        err = max(err, rel(res[0][1], dh1), rel(torch.cat([x[2] for x in res]), dw1))
+        return err
+    vocab_parallel.count = 3
+
     try:
         suite("loss_equivalence", 1e-3, loss_eq)
         suite("gradient_recompute", 1e-2, grads)
         suite("window_sweep", 1e-5, window)
         suite("shard_invariance", 1e-5, shards)
         suite("stability", 1e-4, stability)
+        suite("vocab_parallel_ranks", 1e-3, vocab_parallel)
     except fce.FusedCEError as e:
         print(f"error: {type(e).__name__}: {e}", file=sys.stderr)
         return 2

@@ -64,6 +64,17 @@ struct fce_handle_s {
     int64_t bwd_tma_epi = 3;
     int64_t dh_group = 1;     // bands per dH group in the persistent backward
     int64_t skip_ignored = 1; // compact away ignored rows before the tile kernels
+    int64_t bwd_reserve_sms = 0;  // SMs the persistent backward leaves free (overlapped collectives)
+    int64_t vp_overlap_chunks = 0;  // fce_vp_backward: row chunks whose dH all-reduce overlaps the kernel (0: off)
+    int64_t vp_reserve_sms = 8;     // ... and the SMs the kernel leaves to the collectives
+    int64_t comm_trace_ptr = 0;     // dev only: globaltimer stamps of the overlapped collectives
+    // last persistent backward launch: where each row chunk's dH completion is counted
+    struct LastBwd {
+        bool valid = false;
+        const unsigned* counters = nullptr;
+        int64_t row_chunk = 0, n_rc = 0, bands = 0, n_dh = 0;
+    } last_bwd;
+    cudaEvent_t ctr_reset_ev = nullptr;  // when set: recorded right after the counter reset
     // compaction buffers (grow-only, separate from ws so both can be live)
     void* cws = nullptr;
     size_t cws_size = 0;
@@ -90,6 +101,12 @@ struct fce_handle_s {
 
 namespace fce {
 cudaStream_t handle_stream(fce_handle h) { return h ? h->stream : nullptr; }
+int64_t handle_vp_overlap_chunks(fce_handle h) { return h ? h->vp_overlap_chunks : 0; }
+int64_t handle_vp_reserve_sms(fce_handle h) { return h ? h->vp_reserve_sms : 0; }
+int handle_device(fce_handle h) { return h ? h->device : 0; }
+unsigned long long* handle_comm_trace(fce_handle h) {
+    return h ? reinterpret_cast<unsigned long long*>(h->comm_trace_ptr) : nullptr;
+}
 void set_last_error(const char* msg) { g_last_error = msg; }
 }  // namespace fce
 
@@ -367,6 +384,7 @@ FwdGeom forward_geometry(fce_handle h, const fce_problem* p, int64_t window) {
 
 fce_status run_forward_tiles(fce_handle h, const fce_problem* p, const FwdGeom& g, float* pm, float* pa,
                              float* pzt, uint8_t* pf, const unsigned long long* n_valid = nullptr) {
+    fce::NvtxRange nvtx_("K1 forward tiles (tcgen05, online LSE)");
     TileParams tp;
     std::memset(&tp, 0, sizeof(tp));
     TensorMaps maps;
@@ -408,6 +426,7 @@ fce_status run_backward_persistent(fce_handle h, const fce_problem* p, const flo
                                    float* dhidden, int64_t lddh, float* dweight, int64_t lddw,
                                    int accumulate_dhidden, bool dw_bf16 = false,
                                    const unsigned long long* n_valid = nullptr) {
+    fce::NvtxRange nvtx_("K2 persistent backward (S -> G -> dH, dW)");
     char* ws = static_cast<char*>(h->ws);
     __nv_bfloat16* g_ring = reinterpret_cast<__nv_bfloat16*>(ws + h->bwd_scratch[0]);
     unsigned* d_ctr = reinterpret_cast<unsigned*>(ws + h->bwd_scratch[1]);
@@ -464,6 +483,13 @@ fce_status run_backward_persistent(fce_handle h, const fce_problem* p, const flo
     bp.dw = dweight;
 
     FCE_CUDA(cudaMemsetAsync(d_ctr, 0, sizeof(unsigned) * (1 + 4 * n_chunks + n_chunks * mb_max), h->stream));
+    if (h->ctr_reset_ev) FCE_CUDA(cudaEventRecord(h->ctr_reset_ev, h->stream));
+    h->last_bwd.valid = dhidden != nullptr;
+    h->last_bwd.counters = d_ctr;
+    h->last_bwd.row_chunk = row_chunk;
+    h->last_bwd.n_rc = n_rc;
+    h->last_bwd.bands = n_bd;
+    h->last_bwd.n_dh = bp.n_dh;
     // ring rows past a short last row chunk (up to its 256-row unit edge) are
     // read by dW units and multiplied by zero-filled H rows: keep them finite
     const int64_t nc_last = p->n - (n_rc - 1) * row_chunk;
@@ -499,7 +525,8 @@ fce_status run_backward_persistent(fce_handle h, const fce_problem* p, const flo
     if (dw_bf16 && !(bp.tma_epi & 2))
         return fail(FCE_CUDA_ERROR, "bf16 dW needs the TMA epilogue (16-byte aligned rows)");
     TimedRegion tr(h);
-    cudaError_t e = launch_bwd_persistent(bp, maps, h->sms, h->stream);
+    const int grid = static_cast<int>(std::max<int64_t>(2, h->sms - h->bwd_reserve_sms));
+    cudaError_t e = launch_bwd_persistent(bp, maps, grid, h->stream);
     const double per_row = 2.0 * p->d * p->v * (1 + (dhidden ? 1 : 0) + (dweight ? 1 : 0));
     tr.done(3, per_row * p->n, per_row, n_valid);
     h->launches += 1;
@@ -630,6 +657,17 @@ fce_status fce_set_option(fce_handle h, const char* key, int64_t value) {
     } else if (!std::strcmp(key, "dh_group")) {
         if (value < 1 || value > 64) return fail(FCE_INVALID_ARGUMENT, "dh_group must be in [1, 64]");
         h->dh_group = value;
+    } else if (!std::strcmp(key, "bwd_reserve_sms")) {
+        if (value > h->sms - 2) return fail(FCE_INVALID_ARGUMENT, "bwd_reserve_sms must leave at least one CTA pair");
+        h->bwd_reserve_sms = value;
+    } else if (!std::strcmp(key, "vp_overlap_chunks")) {
+        if (value == 1 || value > 64) return fail(FCE_INVALID_ARGUMENT, "vp_overlap_chunks must be 0 or in [2, 64]");
+        h->vp_overlap_chunks = value;
+    } else if (!std::strcmp(key, "comm_trace_ptr")) {
+        h->comm_trace_ptr = value;
+    } else if (!std::strcmp(key, "vp_reserve_sms")) {
+        if (value > h->sms - 2) return fail(FCE_INVALID_ARGUMENT, "vp_reserve_sms must leave at least one CTA pair");
+        h->vp_reserve_sms = value;
     } else if (!std::strcmp(key, "skip_ignored")) {
         h->skip_ignored = value ? 1 : 0;
     } else if (!std::strcmp(key, "fwd_m_group")) {
@@ -680,6 +718,7 @@ fce_status fce_launch_count(fce_handle h, int64_t* count) {
 
 fce_status fce_forward(fce_handle h, const fce_problem* p, int reduction, int64_t window,
                        fce_stats stats, float* lse, float* loss_rows, float* loss_reduced) {
+    fce::NvtxRange nvtx_("fce_forward");
     fce_status s = check_handle(h);
     if (s) return s;
     if ((s = check_problem(p))) return s;
@@ -728,6 +767,7 @@ fce_status fce_forward(fce_handle h, const fce_problem* p, int reduction, int64_
 }
 
 fce_status fce_forward_partial(fce_handle h, const fce_problem* p, fce_stats partial) {
+    fce::NvtxRange nvtx_("fce_forward_partial");
     fce_status s = check_handle(h);
     if (s) return s;
     if ((s = check_problem(p))) return s;
@@ -780,6 +820,7 @@ fce_status merge_partials(fce_handle h, int parts, int64_t n, int64_t part_strid
                           const float* m, const float* a, const float* z_target, const uint8_t* found,
                           const int64_t* targets, int32_t has_ignore, int64_t ignore_index, int reduction,
                           fce_stats merged, float* lse, float* loss_rows, float* loss_reduced) {
+    fce::NvtxRange nvtx_("fce_merge_partials");
     fce_status s = check_handle(h);
     if (s) return s;
     if (parts <= 0) return fail(FCE_INVALID_LAYOUT, "no partials to merge");
@@ -853,6 +894,7 @@ static fce_status backward_impl(fce_handle h, const fce_problem* p, fce_stats st
                                 float upstream_scalar, const float* upstream_dev, const float* upstream_rows,
                                 void* dhidden_out, int64_t lddh, int dh_dtype, void* dweight_out, int64_t lddw,
                                 int dw_dtype, int accumulate_dhidden) {
+    fce::NvtxRange nvtx_("fce_backward");
     fce_status s = check_handle(h);
     if (s) return s;
     if ((s = check_problem(p))) return s;
@@ -1210,3 +1252,45 @@ fce_status fce_f32_to_bf16(fce_handle h, const float* in, int64_t rows, int64_t 
 }
 
 }  // extern "C"
+
+namespace fce {
+
+fce_status backward_for_overlap(fce_handle h, const fce_problem* p, fce_stats stats, int reduction,
+                                float upstream_scalar, const float* upstream_rows, float* dhidden, int64_t lddh,
+                                float* dweight, int64_t lddw, int64_t row_chunk, int reserve_sms,
+                                cudaEvent_t counters_reset, std::vector<DhChunkDone>* done) {
+    fce_status s = check_handle(h);
+    if (s) return s;
+    if (!h->bwd_persistent || p->has_ignore || !dhidden)
+        return fail(FCE_INVALID_ARGUMENT, "overlapped backward needs the persistent kernel, dH and no ignore_index");
+    const int64_t saved_rc = h->row_chunk, saved_res = h->bwd_reserve_sms;
+    h->row_chunk = round_up(row_chunk, 256);
+    h->bwd_reserve_sms = std::min<int64_t>(reserve_sms, h->sms - 2);
+    h->ctr_reset_ev = counters_reset;
+    h->last_bwd.valid = false;
+    s = backward_impl(h, p, stats, reduction, upstream_scalar, nullptr, upstream_rows, dhidden, lddh, FCE_DTYPE_F32,
+                      dweight, lddw, FCE_DTYPE_F32, 0);
+    h->row_chunk = saved_rc;
+    h->bwd_reserve_sms = saved_res;
+    h->ctr_reset_ev = nullptr;
+    if (s) return s;
+    if (!h->last_bwd.valid) return fail(FCE_INVALID_ARGUMENT, "no persistent backward was launched");
+    const LastBwdView lb{h->last_bwd.counters, h->last_bwd.row_chunk, h->last_bwd.n_rc, h->last_bwd.bands,
+                         h->last_bwd.n_dh};
+    done->clear();
+    for (int64_t rc = 0; rc < lb.n_rc; ++rc) {
+        // dH of a row chunk is final when the dH units of its last vocabulary
+        // band are: dH groups of one row chunk complete in band order (each
+        // waits for the previous one), every unit signals from both CTAs
+        const int64_t c_last = rc * lb.bands + lb.bands - 1;
+        DhChunkDone d;
+        d.counter = lb.counters + 1 + 4 * c_last + 1;
+        d.target = static_cast<unsigned>(2 * lb.n_dh);
+        d.row0 = rc * lb.row_chunk;
+        d.rows = std::min(lb.row_chunk, p->n - d.row0);
+        done->push_back(d);
+    }
+    return FCE_OK;
+}
+
+}  // namespace fce

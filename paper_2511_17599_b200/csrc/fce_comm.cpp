@@ -93,12 +93,15 @@ public:
         return comm_fail(FCE_NCCL_ERROR, "%s: %s", what, nccl().error_string(r));
     }
     fce_status all_gather(const void* send, void* recv, size_t bytes, cudaStream_t s) override {
+        NvtxRange nvtx_("nccl all_gather");
         return check(nccl().all_gather(send, recv, bytes, ncclUint8, comm, s), "ncclAllGather");
     }
     fce_status all_reduce_sum(const float* send, float* recv, size_t count, cudaStream_t s) override {
+        NvtxRange nvtx_("nccl all_reduce");
         return check(nccl().all_reduce(send, recv, count, ncclFloat32, ncclSum, comm, s), "ncclAllReduce");
     }
     fce_status reduce_scatter_sum(const float* send, float* recv, size_t recv_count, cudaStream_t s) override {
+        NvtxRange nvtx_("nccl reduce_scatter");
         return check(nccl().reduce_scatter(send, recv, recv_count, ncclFloat32, ncclSum, comm, s),
                      "ncclReduceScatter");
     }
@@ -237,6 +240,7 @@ public:
     }
 
     fce_status all_gather(const void* send, void* recv, size_t bytes, cudaStream_t s) override {
+        NvtxRange nvtx_("local all_gather");
         publish(send, recv);
         fce_status st = sync_phase(0, s);
         if (st) return st;
@@ -250,6 +254,7 @@ public:
     }
 
     fce_status all_reduce_sum(const float* send, float* recv, size_t count, cudaStream_t s) override {
+        NvtxRange nvtx_("local all_reduce");
         publish(send, recv);
         fce_status st = sync_phase(0, s);
         if (st) return st;
@@ -272,6 +277,7 @@ public:
     }
 
     fce_status reduce_scatter_sum(const float* send, float* recv, size_t recv_count, cudaStream_t s) override {
+        NvtxRange nvtx_("local reduce_scatter");
         publish(send, recv);
         fce_status st = sync_phase(0, s);
         if (st) return st;

@@ -7,9 +7,13 @@
 // buffers (same device, or a peer device with P2P access over NVLink); the
 // kernel is pure HBM streaming: (k + 1) x 4 B per element, 16-byte vector
 // loads when every pointer allows it.
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
 #include <cstdint>
 
 #include "fce_comm.h"
+#include "fce_internal.h"
 
 namespace fce {
 
@@ -60,6 +64,51 @@ cudaError_t launch_sum_peers(const PeerPtrs& src, int k, float* dst, size_t coun
         const int blocks = static_cast<int>(want < static_cast<size_t>(4 * sms) ? want : 4 * sms);
         k_sum_peers<<<blocks, 256, 0, s>>>(src, k, dst, done, count);
     }
+    return cudaGetLastError();
+}
+
+// ------------------------------------------------ stream wait on a device counter
+// The overlapped vocab-parallel backward releases the collective of a row chunk
+// from the comm stream as soon as the persistent kernel's dependency counter
+// says the chunk's dH rows are final.  cuStreamWaitValue32 holds the stream in
+// the front end (no SM is occupied); where stream memory operations are not
+// available a one-thread kernel spins on the counter instead.
+__global__ void k_wait_geq(const unsigned* counter, unsigned target) {
+    unsigned v;
+    for (;;) {
+        asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(counter) : "memory");
+        if (v >= target) break;
+        __nanosleep(1000);
+    }
+}
+
+cudaError_t stream_wait_geq(cudaStream_t s, const unsigned* counter, unsigned target) {
+    // function-local static: resolved once (the driver entry point; no -lcuda)
+    static const PFN_cuStreamWaitValue32_v8000 fn = [] {
+        cudaDriverEntryPointQueryResult q;
+        void* ptr = nullptr;
+        if (cudaGetDriverEntryPoint("cuStreamWaitValue32", &ptr, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            return reinterpret_cast<PFN_cuStreamWaitValue32_v8000>(ptr);
+        return static_cast<PFN_cuStreamWaitValue32_v8000>(nullptr);
+    }();
+    if (fn) {
+        CUresult r = fn(s, reinterpret_cast<CUdeviceptr>(counter), target, CU_STREAM_WAIT_VALUE_GEQ);
+        if (r == CUDA_SUCCESS) return cudaSuccess;  // else (memory ops unsupported): spin kernel
+    }
+    k_wait_geq<<<1, 1, 0, s>>>(counter, target);
+    return cudaGetLastError();
+}
+
+// globaltimer stamp when the stream reaches this point (device traces)
+__global__ void k_stamp(unsigned long long* slot) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    *slot = t;
+}
+
+cudaError_t launch_stamp(cudaStream_t s, unsigned long long* slot) {
+    k_stamp<<<1, 1, 0, s>>>(slot);
     return cudaGetLastError();
 }
 

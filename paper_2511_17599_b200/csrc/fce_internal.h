@@ -3,13 +3,26 @@
 #pragma once
 
 #include <cstdint>
+#include <vector>
 #include <cuda.h>
 #include <cuda_runtime.h>
 #include <cuda_bf16.h>
 
+#include <nvtx3/nvToolsExt.h>
+
 #include "../../include/fce/fce.h"
 
 namespace fce {
+
+// NVTX range around a host entry point / launch group (header-only NVTX3:
+// free when no profiler is attached; nsys / ncu --nvtx show the K1 / K2 /
+// collective phases of a step).
+struct NvtxRange {
+    explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+    ~NvtxRange() { nvtxRangePop(); }
+    NvtxRange(const NvtxRange&) = delete;
+    NvtxRange& operator=(const NvtxRange&) = delete;
+};
 
 // Tile geometry of the tcgen05 kernel (one CTA per SM, 1-CTA UMMA).
 constexpr int kBM = 128;      // rows per tile = TMEM lanes
@@ -121,8 +134,37 @@ fce_status merge_partials(fce_handle h, int parts, int64_t n, int64_t part_strid
                           const int64_t* targets, int32_t has_ignore, int64_t ignore_index, int reduction,
                           fce_stats merged, float* lse, float* loss_rows, float* loss_reduced);
 
+// Overlapped vocab-parallel backward (fce_api.cpp): fce_backward with the rows
+// cut into row chunks of `row_chunk`, the persistent kernel leaving
+// `reserve_sms` SMs free for collectives, `counters_reset` recorded on the
+// handle stream once the dependency counters are zeroed, and for every row
+// chunk the device counter + value that mark its dH rows final.
+struct DhChunkDone {
+    const unsigned* counter;
+    unsigned target;
+    int64_t row0, rows;
+};
+struct LastBwdView {
+    const unsigned* counters;
+    int64_t row_chunk, n_rc, bands, n_dh;
+};
+fce_status backward_for_overlap(fce_handle h, const fce_problem* p, fce_stats stats, int reduction,
+                                float upstream_scalar, const float* upstream_rows, float* dhidden, int64_t lddh,
+                                float* dweight, int64_t lddw, int64_t row_chunk, int reserve_sms,
+                                cudaEvent_t counters_reset, std::vector<DhChunkDone>* done);
+// Stream-ordered wait until *counter >= target (cuStreamWaitValue32, or a
+// one-thread spin kernel where stream memory operations are unavailable).
+cudaError_t stream_wait_geq(cudaStream_t s, const unsigned* counter, unsigned target);
+
 // Stream a handle launches on (fce_api.cpp).
 cudaStream_t handle_stream(fce_handle h);
+int handle_device(fce_handle h);
+// Options "vp_overlap_chunks" / "vp_reserve_sms" of the handle (fce_vp_backward).
+int64_t handle_vp_overlap_chunks(fce_handle h);
+int64_t handle_vp_reserve_sms(fce_handle h);
+// Option "comm_trace_ptr" (dev): u64 slots for globaltimer stamps, 2 per chunk.
+unsigned long long* handle_comm_trace(fce_handle h);
+cudaError_t launch_stamp(cudaStream_t s, unsigned long long* slot);
 // Thread-local message returned by fce_last_error (fce_api.cpp).
 void set_last_error(const char* msg);
 

@@ -32,6 +32,9 @@ struct fce_comm_s {
     size_t buf_size = 0;
     int64_t* xchg = nullptr;   // small exchange area: [4] send + [4 * nranks] recv
     int64_t* xchg_host = nullptr;
+    // overlapped backward: the collectives' stream and its two fences
+    cudaStream_t comm_stream = nullptr;
+    cudaEvent_t reset_ev = nullptr, done_ev = nullptr;
 };
 
 struct fce_comm_group_s {
@@ -112,6 +115,50 @@ fce_status copy_rows(void* dst, size_t ld_dst_bytes, const void* src, size_t ld_
     return FCE_OK;
 }
 
+// tp_backward with the dH all-reduce overlapped with the kernel
+// (parallel_sim.hpp:276-288 reduces dH after every rank's shard is done; here
+// the rows are cut into `chunks` row chunks and chunk c's all-reduce runs on the
+// communicator's stream while the persistent kernel computes chunk c + 1).
+// The comm stream starts after the kernel's dependency counters are reset,
+// then waits on the device counter that marks each chunk's dH rows final; the
+// kernel leaves vp_reserve_sms SMs free so the collective's kernels run beside
+// it.  The handle stream resumes after the last collective.
+fce_status vp_backward_overlapped(fce_handle h, fce_comm c, const fce_problem* p, fce_stats merged, int reduction,
+                                  float upstream_scalar, const float* upstream_rows, float* dhidden,
+                                  float* dweight_shard, int64_t lddw, int64_t chunks) {
+    cudaStream_t stream = fce::handle_stream(h);
+    VP_CUDA(cudaSetDevice(fce::handle_device(h)));
+    if (!c->comm_stream) {
+        int lo = 0, hi = 0;
+        VP_CUDA(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+        VP_CUDA(cudaStreamCreateWithPriority(&c->comm_stream, cudaStreamNonBlocking, hi));
+        VP_CUDA(cudaEventCreateWithFlags(&c->reset_ev, cudaEventDisableTiming));
+        VP_CUDA(cudaEventCreateWithFlags(&c->done_ev, cudaEventDisableTiming));
+    }
+    // the comm stream follows everything already queued (inputs of the reduce)
+    VP_CUDA(cudaEventRecord(c->done_ev, stream));
+    VP_CUDA(cudaStreamWaitEvent(c->comm_stream, c->done_ev, 0));
+    std::vector<fce::DhChunkDone> done;
+    const int64_t row_chunk = (p->n + chunks - 1) / chunks;
+    fce_status s = fce::backward_for_overlap(h, p, merged, reduction, upstream_scalar, upstream_rows, dhidden, p->d,
+                                             dweight_shard, lddw, row_chunk,
+                                             static_cast<int>(fce::handle_vp_reserve_sms(h)), c->reset_ev, &done);
+    if (s) return s;
+    VP_CUDA(cudaStreamWaitEvent(c->comm_stream, c->reset_ev, 0));
+    unsigned long long* trace = fce::handle_comm_trace(h);
+    for (size_t i = 0; i < done.size(); ++i) {
+        const fce::DhChunkDone& d = done[i];
+        VP_CUDA(fce::stream_wait_geq(c->comm_stream, d.counter, d.target));
+        if (trace) VP_CUDA(fce::launch_stamp(c->comm_stream, trace + 2 * i));
+        float* rows = dhidden + d.row0 * p->d;
+        if ((s = c->impl->all_reduce_sum(rows, rows, static_cast<size_t>(d.rows) * p->d, c->comm_stream))) return s;
+        if (trace) VP_CUDA(fce::launch_stamp(c->comm_stream, trace + 2 * i + 1));
+    }
+    VP_CUDA(cudaEventRecord(c->done_ev, c->comm_stream));
+    VP_CUDA(cudaStreamWaitEvent(stream, c->done_ev, 0));
+    return FCE_OK;
+}
+
 }  // namespace
 
 extern "C" {
@@ -175,6 +222,9 @@ fce_status fce_comm_destroy(fce_comm c) {
     if (c->buf) cudaFree(c->buf);
     if (c->xchg) cudaFree(c->xchg);
     if (c->xchg_host) cudaFreeHost(c->xchg_host);
+    if (c->comm_stream) cudaStreamDestroy(c->comm_stream);
+    if (c->reset_ev) cudaEventDestroy(c->reset_ev);
+    if (c->done_ev) cudaEventDestroy(c->done_ev);
     delete c->impl;
     delete c;
     return FCE_OK;
@@ -215,6 +265,7 @@ fce_status fce_comm_reduce_scatter_f32(fce_handle h, fce_comm c, const float* se
 
 fce_status fce_vp_forward(fce_handle h, fce_comm c, const fce_problem* p, int reduction, fce_stats merged,
                           float* lse, float* loss_rows, float* loss_reduced) {
+    fce::NvtxRange nvtx_("fce_vp_forward");
     fce_status s = check_args(h, c);
     if (s) return s;
     if (!p) return vp_fail(FCE_INVALID_ARGUMENT, "null problem");
@@ -240,6 +291,7 @@ fce_status fce_vp_forward(fce_handle h, fce_comm c, const fce_problem* p, int re
 fce_status fce_vp_backward(fce_handle h, fce_comm c, const fce_problem* p, fce_stats merged, int reduction,
                            float upstream_scalar, const float* upstream_rows, float* dhidden, int64_t lddh,
                            float* dweight_shard, int64_t lddw) {
+    fce::NvtxRange nvtx_("fce_vp_backward");
     fce_status s = check_args(h, c);
     if (s) return s;
     if (!p) return vp_fail(FCE_INVALID_ARGUMENT, "null problem");
@@ -248,6 +300,10 @@ fce_status fce_vp_backward(fce_handle h, fce_comm c, const fce_problem* p, fce_s
                             lddw, 0);
     if (lddh < p->d) return vp_fail(FCE_DIMENSION_MISMATCH, "lddh < d");
     cudaStream_t stream = fce::handle_stream(h);
+    const int64_t chunks = fce::handle_vp_overlap_chunks(h);
+    if (chunks > 1 && lddh == p->d && !p->has_ignore && p->n >= 256 * chunks)
+        return vp_backward_overlapped(h, c, p, merged, reduction, upstream_scalar, upstream_rows, dhidden,
+                                      dweight_shard, lddw, chunks);
     // a strided dH is reduced through a packed [n, d] buffer (one collective)
     float* dst = dhidden;
     if (lddh != p->d) {
@@ -267,6 +323,7 @@ fce_status fce_vp_backward(fce_handle h, fce_comm c, const fce_problem* p, fce_s
 
 fce_status fce_sp_gather(fce_handle h, fce_comm c, const void* shard, int64_t shard_rows, int64_t ld_shard,
                          int64_t d, int64_t n_total, void* full, int64_t ld_full) {
+    fce::NvtxRange nvtx_("fce_sp_gather");
     fce_status s = check_args(h, c);
     if (s) return s;
     if (d <= 0 || n_total <= 0) return vp_fail(FCE_EMPTY_INPUT, "sp gather requires d > 0 and N > 0");
@@ -304,6 +361,7 @@ fce_status fce_sp_gather(fce_handle h, fce_comm c, const void* shard, int64_t sh
 
 fce_status fce_sp_scatter(fce_handle h, fce_comm c, const float* dh_partial, int64_t n_total, int64_t lddh,
                           int64_t d, float* dh_shard, int64_t shard_rows, int64_t ld_shard) {
+    fce::NvtxRange nvtx_("fce_sp_scatter");
     fce_status s = check_args(h, c);
     if (s) return s;
     if (d <= 0 || n_total <= 0) return vp_fail(FCE_EMPTY_INPUT, "sp scatter requires d > 0 and N > 0");
@@ -344,6 +402,7 @@ fce_status fce_sp_scatter(fce_handle h, fce_comm c, const float* dh_partial, int
 
 fce_status fce_dp_step(fce_handle h, fce_comm c, const fce_problem* p, int reduction, float* loss, float* dhidden,
                        int64_t lddh, float* dweight, int64_t lddw) {
+    fce::NvtxRange nvtx_("fce_dp_step");
     fce_status s = check_args(h, c);
     if (s) return s;
     if (!p || !loss || !dweight) return vp_fail(FCE_INVALID_ARGUMENT, "null problem, loss or dW");

@@ -1,14 +1,18 @@
 """Summarise ncu captures into profiles/ (dev tool).
 
-usage: python scripts/ncu_summary.py <round-tag> <launches.csv> <full.ncu-rep> [bench.json]
+usage: python scripts/ncu_summary.py <round-tag> <config> <launches.csv> <full.ncu-rep> [bench.json]
 Writes profiles/<tag>_launches.csv (copy), profiles/<tag>_ncu_summary.md and
-profiles/traffic.json (DRAM bytes per launch of each kernel, read by bench.py).
+profiles/traffic.json: DRAM bytes per launch of each kernel of <config>, with
+the hash of the kernel sources captured (bench.py reports the number only
+while the sources are unchanged).
 """
 import collections, csv, io, json, os, shutil, subprocess, sys
 
-tag, launches, rep = sys.argv[1:4]
-bench = json.load(open(sys.argv[4])) if len(sys.argv) > 4 else None
+tag, config, launches, rep = sys.argv[1:5]
+bench = json.load(open(sys.argv[5])) if len(sys.argv) > 5 else None
 root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, root)
+from bench import _source_hash  # noqa: E402
 prof = os.path.join(root, "profiles")
 os.makedirs(prof, exist_ok=True)
 shutil.copy(launches, os.path.join(prof, f"{tag}_launches.csv"))
@@ -51,7 +55,7 @@ want = {
 }
 scale = {"Gbyte": 1e9, "Mbyte": 1e6, "Kbyte": 1e3, "byte": 1.0, "Tbyte": 1e12}
 traffic = {}
-lines = [f"# ncu summary — {tag}", "",
+lines = [f"# ncu summary — {tag} ({config})", "",
          "Captured under gpurun on one B200 with `--clock-control none` (cold cache, serialised",
          "launches: compare shares, not absolute times with the bench).", "",
          "## Launch list (one fwd+bwd step, `ncu --metrics gpu__time_duration.sum`)", "",
@@ -80,6 +84,9 @@ if bench:
 open(os.path.join(prof, f"{tag}_ncu_summary.md"), "w").write("\n".join(lines))
 tp = os.path.join(prof, "traffic.json")
 old = json.load(open(tp)) if os.path.exists(tp) else {}
-old.update({k: v for k, v in traffic.items()})
+old = {k: v for k, v in old.items() if isinstance(v, dict)}  # drop the round-1 flat format
+sha = _source_hash()
+old[config] = {k: {"dram_bytes": v, "source_sha": sha, "capture": f"{tag}_ncu_summary.md"}
+               for k, v in traffic.items()}
 json.dump(old, open(tp, "w"), indent=1)
 print("\n".join(lines[:40]))

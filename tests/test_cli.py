@@ -24,7 +24,8 @@ def test_usage_errors_exit_2():
 def test_verify_passes(cuda):
     r = run("verify", "--loss-instances", "12", "--grad-instances", "4")
     assert r.returncode == 0, r.stdout + r.stderr
-    for suite in ("loss_equivalence", "gradient_recompute", "window_sweep", "shard_invariance", "stability"):
+    for suite in ("loss_equivalence", "gradient_recompute", "window_sweep", "shard_invariance", "stability",
+                  "vocab_parallel_ranks"):
         assert suite in r.stdout
     assert "overall: PASS" in r.stdout
 
@@ -41,3 +42,22 @@ def test_bench_csv_schema(cuda, tmp_path):
     assert len(lines) == 5 and all(len(l.split(",")) == 10 for l in lines)
     losses = [float(l.split(",")[9]) for l in lines[1:]]
     assert max(losses) - min(losses) < 1e-3 * abs(losses[0])  # every method computes the same loss
+
+
+@pytest.mark.gpu
+def test_bench_losses_match_the_oracle(cuda, tmp_path):
+    """The CLI's device results against the CPU oracle on the same seeded
+    instance (the CLI draws make_random_instance bit for bit on the device)."""
+    sys.path.insert(0, ROOT)
+    from oracle import bindings as ob
+    out = tmp_path / "b.csv"
+    r = run("bench", "--bt", "200,333", "--vocab", "1500", "--hidden", "136", "--repeats", "1", "--warmup", "0",
+            "--methods", "fused,fused_windowed,fused_partial_grad", "--window", "384", "--reduction", "sum",
+            "--seed", "7", "--output", str(out))
+    assert r.returncode == 0, r.stderr
+    for line in out.read_text().strip().splitlines()[1:]:
+        bt, vocab, hidden, method = line.split(",")[:4]
+        loss = float(line.split(",")[9])
+        H, W, Y = ob.make_instance(int(bt), int(hidden), int(vocab), 7)
+        _, _, ref = ob.forward(H, W, Y, "sum")
+        assert abs(loss - ref) <= 1e-3 * abs(ref), (method, bt, loss, ref)

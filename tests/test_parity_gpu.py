@@ -351,6 +351,47 @@ def test_large_offset_stability(cuda):
     assert np.all(out.stats.m.cpu().numpy() > 10000)
 
 
+@pytest.mark.parametrize("ign,red", [(-1, "mean"), (-5, "sum"), (-7, "none"), (-100, "mean")])
+def test_ignore_sentinels(cuda, ign, red):
+    """The ignore sentinels the reference tests use (-100, -1, -5, -7; e.g.
+    test_reference.cpp:93-109, test_fused_backward.cpp:212-245): any negative
+    sentinel is matched exactly, its rows get identity stats, zero loss and
+    zero dH, and no other negative id is accepted."""
+    n, d, v = 257, 72, 900
+    H, W, Y = ob.make_instance(n, d, v, 77, ign, 0.3)
+    assert (Y == ign).any()
+    st, rows, lred = ob.forward(H, W, Y, red, ign)
+    Hd, Wd, Yd = to_dev(H, W, Y)
+    out = fce.fused_forward(Hd, Wd, Yd, red, ign)
+    check_forward(out, st, rows, lred, Y, ign, red)
+    up = np.linspace(0.5, 1.5, n).astype(np.float32) if red == "none" else 1.0
+    dH, dW = ob.backward(H, W, Y, st, red, up, ign)
+    dh, dw = fce.fused_backward_recompute(Hd, Wd, Yd, out.stats, red,
+                                          torch.from_numpy(up).cuda() if red == "none" else 1.0, ign)
+    check_grads(dh, dw, dH, dW, Y, ign)
+    # a different negative id is out of range, not ignored
+    Y2 = Y.copy()
+    Y2[Y2 == ign] = ign - 1
+    with pytest.raises(fce.TargetOutOfRange):
+        fce.fused_forward(Hd, Wd, torch.from_numpy(Y2).cuda(), red, ign)
+
+
+def test_zero_hidden_gives_uniform_probability_gradient(cuda):
+    """test_reference.cpp:197-216 on the device path: H = 0 makes every logit 0,
+    so p = 1/V, loss = ln V, dW = 0 exactly and dH[n] = sum_v (1/V - 1[v=y]) W_v."""
+    n, d, v = 64, 136, 1000
+    _, W, Y = ob.make_instance(n, d, v, 29)
+    H = np.zeros((n, d), np.float32)
+    Hd, Wd, Yd = to_dev(H, W, Y)
+    out = fce.fused_forward(Hd, Wd, Yd, "sum")
+    assert abs(out.loss.item() - n * math.log(v)) <= 1e-5 * n * math.log(v)
+    dh, dw = fce.fused_backward_recompute(Hd, Wd, Yd, out.stats, "sum", 1.0)
+    assert torch.count_nonzero(dw).item() == 0
+    Wn = W.astype(np.float64)
+    expect = Wn.mean(0)[None, :] - Wn[Y]
+    assert relmax(dh.cpu().numpy(), expect) < GRAD_RTOL
+
+
 def test_all_ignored_mean_is_zero_with_zero_grads(cuda):
     # test_reference.cpp:111-130
     H, W, _ = ob.make_instance(40, 16, 100, 11)
