@@ -16,8 +16,9 @@ ORACLE    := oracle/liboracle.so
 REF_LIB   := oracle/_ref/libfce_ref.so
 
 DROPIN_TEST := tests/cpp/test_dropin
+DROPIN_BENCH := tests/cpp/bench_dropin
 
-all: $(LIB) $(ORACLE) ref $(DROPIN_TEST)
+all: $(LIB) $(ORACLE) ref $(DROPIN_TEST) $(DROPIN_BENCH)
 
 # C++ drop-in API (include/fusedce) against the oracle; runs on a B200
 $(DROPIN_TEST): tests/cpp/test_dropin.cpp $(wildcard include/fusedce/*.hpp include/fusedce/detail/*.hpp) \
@@ -25,6 +26,12 @@ $(DROPIN_TEST): tests/cpp/test_dropin.cpp $(wildcard include/fusedce/*.hpp inclu
 	$(CXX) -std=c++20 -O2 -Iinclude -I/usr/local/cuda/include -o $@ tests/cpp/test_dropin.cpp \
 	    -L$(PKG) -lfce -Loracle -loracle -L/usr/local/cuda/lib64 -lcudart \
 	    -Wl,-rpath,'$$ORIGIN/../../$(PKG)' -Wl,-rpath,'$$ORIGIN/../../oracle' -Wl,-rpath,/usr/local/cuda/lib64
+
+$(DROPIN_BENCH): tests/cpp/bench_dropin.cpp $(wildcard include/fusedce/*.hpp include/fusedce/detail/*.hpp) \
+                 include/fce/fce.h $(LIB)
+	$(CXX) -std=c++20 -O2 -Iinclude -I/usr/local/cuda/include -o $@ tests/cpp/bench_dropin.cpp \
+	    -L$(PKG) -lfce -L/usr/local/cuda/lib64 -lcudart \
+	    -Wl,-rpath,'$$ORIGIN/../../$(PKG)' -Wl,-rpath,/usr/local/cuda/lib64
 
 $(LIB): $(CSRC)/fce_kernels.cu $(CSRC)/fce_bwd.cu $(CSRC)/fce_pair.cu $(CSRC)/fce_fwd_pair.cu $(CSRC)/fce_api.cpp $(CSRC)/fce_vp.cpp $(CSRC)/fce_internal.h \
         $(CSRC)/fce_comm.cpp $(CSRC)/fce_comm.cu $(CSRC)/fce_comm.h include/fce/fce_vp.h \
@@ -47,6 +54,6 @@ $(REF_LIB): oracle/ref_shim.cpp
 	    -I$(REF_DIR)/include -o $@ oracle/ref_shim.cpp
 
 clean:
-	rm -f $(LIB) $(ORACLE) $(REF_LIB) $(DROPIN_TEST)
+	rm -f $(LIB) $(ORACLE) $(REF_LIB) $(DROPIN_TEST) $(DROPIN_BENCH)
 
 .PHONY: all ref clean

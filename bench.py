@@ -541,6 +541,8 @@ def bench_rank(ctx, args):
     }
     if e2e_g:
         line["e2e_with_grads"] = e2e_g
+    if world == 1 and not args.no_dropin:
+        line["e2e_dropin_cpp"] = _dropin_e2e(n, d, v) if frac == 0 else None
     if world == 1 and not args.no_cpu_baseline:
         try:
             line["cpu_baseline"] = cpu_baseline(args.config)
@@ -548,6 +550,22 @@ def bench_rank(ctx, args):
             line["cpu_baseline"] = {"value": None, "unit": "tokens/s", "cores": os.cpu_count(),
                                     "kind": "reference", "sample": f"failed: {exc!r}"}
     return line
+
+
+def _dropin_e2e(n, d, v):
+    """The drop-in C++ API (fusedce::fused_forward + fused_backward_recompute)
+    with host buffers at this shape (tests/cpp/bench_dropin, built by make): the
+    switch-the-include-path user's end-to-end number, uploads and owning host
+    results (dH, dW) included."""
+    exe = os.path.join(ROOT, "tests", "cpp", "bench_dropin")
+    if not os.path.exists(exe):
+        return {"value": None, "note": "tests/cpp/bench_dropin not built"}
+    try:
+        r = subprocess.run([exe, str(n), str(d), str(v), "2"], capture_output=True, text=True, timeout=600)
+        out = [l for l in r.stdout.splitlines() if l.startswith("{")]
+        return json.loads(out[-1]) if r.returncode == 0 and out else {"value": None, "note": r.stderr[-300:]}
+    except Exception as exc:  # never lose the GPU line over this leg
+        return {"value": None, "note": repr(exc)}
 
 
 def _traffic_from_profile(cfg, kernel):
@@ -597,6 +615,7 @@ def main():
     ap.add_argument("--impl", default="fce", choices=["fce", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e-grads", action="store_true")
+    ap.add_argument("--no-dropin", action="store_true", help="skip the C++ drop-in API end-to-end leg")
     ap.add_argument("--e2e-steps", type=int, default=16)
     ap.add_argument("--transport", default="auto", choices=["auto", "nccl", "local"],
                     help="N > 1 without torchrun: NCCL processes (needs N GPUs) or in-process local ranks")

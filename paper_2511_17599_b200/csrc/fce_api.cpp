@@ -950,12 +950,16 @@ static fce_status backward_impl(fce_handle h, const fce_problem* p, fce_stats st
     int64_t band = h->band_cols;
     if (!band) {
         if (h->bwd_persistent) {
-            // 3072 columns from 16384 rows up; shorter row chunks take wider bands
-            // (fewer dH passes, more units per phase): 3072 * sqrt(16384 / rows),
-            // to a multiple of 1024.  Measured best at 1024 / 4096 / 8192 /
-            // 16384 rows: 12288 / 6144 / 6144 / 3072-4096 (profiles/r01_band_small.log).
+            // Base band by width (interleaved A/B on B200, profiles/r02_band_ab.log):
+            // D <= 3072 (Gemma-2-2B) 4096; long row chunks at D >= 6144
+            // (Llama-3-70B) 3072; otherwise (Llama-3-8B, Qwen2.5-7B) 3584.
+            // Shorter row chunks take wider bands (fewer dH passes, more units
+            // per phase): 3072 * sqrt(16384 / rows) to a multiple of 1024,
+            // measured best at 1024 / 4096 / 8192 rows: 12288 / 6144 / 6144
+            // (profiles/r01_band_small.log).
+            const int64_t base = p->d <= 3072 ? 4096 : (row_chunk >= 32768 && p->d >= 6144) ? 3072 : 3584;
             const double w = 3072.0 * std::sqrt(16384.0 / static_cast<double>(row_chunk));
-            band = std::max<int64_t>(3072, static_cast<int64_t>(std::llround(w / 1024.0)) * 1024);
+            band = std::max<int64_t>(base, static_cast<int64_t>(std::llround(w / 1024.0)) * 1024);
         } else {
             // ~32 MB of G per chunk so it stays L2 resident between producer and consumers
             band = std::max<int64_t>(kBN, ((int64_t(16) << 20) / row_chunk) / kBN * kBN);

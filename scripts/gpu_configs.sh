@@ -2,7 +2,7 @@
 set -x
 TAG=${TAG:-r02}
 for c in ${CONFIGS:-llama3-8b qwen2.5-7b gemma2-2b llama3-70b}; do
-  extra="--no-cpu-baseline"
+  extra="--no-cpu-baseline --no-dropin"
   [ "$c" = "llama3-8b" ] && extra=""
   timeout 900 python bench.py --config $c --steps 10 --warmup 3 $extra > gpurun_out/${TAG}_bench_$c.json 2> gpurun_out/${TAG}_bench_$c.err
   timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --profile-from-start off --csv \

@@ -74,7 +74,8 @@ for r in kd:
     try:
         rd = float(r[h2.index("dram__bytes_read.sum")]) * scale.get(units[h2.index("dram__bytes_read.sum")], 1)
         wr = float(r[h2.index("dram__bytes_write.sum")]) * scale.get(units[h2.index("dram__bytes_write.sum")], 1)
-        traffic[name] = rd + wr
+        if rd == rd and wr == wr:  # ncu reports NaN for some very long launches
+            traffic[name] = rd + wr
         lines.append(f"- DRAM traffic per launch: {(rd + wr) / 1e9:.2f} GB")
     except (ValueError, KeyError):
         pass
