@@ -570,9 +570,9 @@ def _dropin_e2e(n, d, v):
 
 def _traffic_from_profile(cfg, kernel):
     """DRAM bytes per launch of the dominant kernel from the committed ncu
-    capture of the CURRENT kernel sources (profiles/traffic.json records the
-    hash of csrc/*.cu|*.cuh it was captured on; a stale entry is not
-    reported)."""
+    capture of the CURRENT sources (profiles/traffic.json records the hash of
+    csrc/* it was captured on — kernels and the host launch plans; a stale
+    entry is not reported)."""
     tpath = os.path.join(ROOT, "profiles", "traffic.json")
     if not os.path.exists(tpath):
         return None
@@ -594,7 +594,7 @@ def _source_hash():
     hsh = hashlib.sha256()
     csrc = os.path.join(ROOT, "paper_2511_17599_b200", "csrc")
     for name in sorted(os.listdir(csrc)):
-        if name.endswith((".cu", ".cuh")):
+        if name.endswith((".cu", ".cuh", ".h", ".cpp")):
             with open(os.path.join(csrc, name), "rb") as f:
                 hsh.update(f.read())
     return hsh.hexdigest()[:16]
