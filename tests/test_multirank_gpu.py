@@ -289,3 +289,42 @@ def test_overlapped_dh_all_reduce_matches_oracle(cuda, k, chunks):
         np.testing.assert_array_equal(dh.cpu().numpy(), res[0][0].cpu().numpy())
     dw_all = np.concatenate([x[1].cpu().numpy() for x in res])
     assert relmax(dw_all, dW) < GRAD_RTOL
+
+
+@pytest.mark.parametrize("case", range(8))
+def test_random_multirank_cases(cuda, case):
+    """Randomised k-rank vocab-parallel steps (k, shapes, reduction, ignore
+    sentinel, overlap option) against the oracle on every rank."""
+    rng = np.random.default_rng(500 + case)
+    k = int(rng.integers(2, 7))
+    n = int(rng.integers(1, 700))
+    d = int(rng.integers(1, 300))
+    v = int(rng.integers(k, 3000))
+    red = ("mean", "sum", "none")[case % 3]
+    ign = (None, -100, -1, -5)[case % 4]
+    frac = 0.0 if ign is None else float(rng.uniform(0.05, 0.5))
+    chunks = 2 if (case % 2 and ign is None and n >= 512) else 0
+    H, W, Y = ob.make_instance(n, d, v, 900 + case, -100 if ign is None else ign, frac)
+    up = rng.standard_normal(n).astype(np.float32) if red == "none" else 1.0
+    Hd, Wd, Yd = bf16(H), bf16(W), torch.from_numpy(Y).cuda()
+    upd = torch.from_numpy(up).cuda() if red == "none" else 1.0
+    ranges = fce.shard_ranges(v, k)
+
+    def rank_fn(r, comm, h):
+        lo, hi = ranges[r]
+        h.set_option("vp_overlap_chunks", chunks)
+        out = vp.native_forward(comm, Hd, Wd[lo:hi], Yd, lo, v, red, ign, handle=h)
+        dh, dw = vp.native_backward(comm, Hd, Wd[lo:hi], Yd, lo, v, out.stats, red, upd, ign, handle=h)
+        return out, dh, dw
+
+    res = vp.run_ranks(k, rank_fn)
+    st, rows, lred = ob.forward(H, W, Y, red, ign)
+    dH, dW = ob.backward(H, W, Y, st, red, up, ign)
+    for out, dh, dw in res:
+        np.testing.assert_array_equal(out.stats.found.cpu().numpy(), st["found"])
+        got = out.loss_rows.cpu().numpy()
+        assert np.max(np.abs(got - rows) / np.maximum(1, np.abs(rows))) < LOSS_RTOL
+        if red != "none":
+            assert abs(out.loss.item() - lred) <= LOSS_RTOL * max(1.0, abs(lred))
+        assert relmax(dh.cpu().numpy(), dH) < GRAD_RTOL
+    assert relmax(np.concatenate([x[2].cpu().numpy() for x in res]), dW) < GRAD_RTOL
