@@ -251,16 +251,25 @@ class DistCtx:
         import torch
         import torch.distributed as dist
         from paper_2511_17599_b200 import vocab_parallel as vp
+        # FCE_BENCH_TRANSPORT=ipc: libfce's own collectives over CUDA IPC peer
+        # memory (ranks may share a GPU), gloo only for the launcher's barrier
+        self.transport = os.environ.get("FCE_BENCH_TRANSPORT", "nccl")
+        if self.transport == "ipc":
+            local = local % max(torch.cuda.device_count(), 1)
         self.world, self.rank, self.device = world, rank, local
         torch.cuda.set_device(local)
         self.stream = torch.cuda.current_stream(local)
         self.dist = None
         self.comm = None
         if world > 1 or force_vp:
-            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-            self.dist = dist
-            self.comm = vp.NativeComm.from_torch_distributed(local)
-        self.transport = "nccl"
+            if self.transport == "ipc":
+                dist.init_process_group("gloo")
+                self.dist = dist
+                self.comm = vp.NativeComm.from_torch_distributed_ipc(local)
+            else:
+                dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+                self.dist = dist
+                self.comm = vp.NativeComm.from_torch_distributed(local)
 
     def barrier(self):
         import torch
@@ -273,7 +282,7 @@ class DistCtx:
         import torch
         if not self.dist:
             return x
-        t = torch.tensor([x], device=f"cuda:{self.device}")
+        t = torch.tensor([x], device="cpu" if self.transport == "ipc" else f"cuda:{self.device}")
         self.dist.all_reduce(t, op=self.dist.ReduceOp.MAX)
         return t.item()
 
@@ -494,6 +503,9 @@ def bench_rank(ctx, args):
         par = "single GPU"
     elif ctx.transport == "nccl":
         par = f"vocab-parallel x{world} (NCCL, one process per GPU)"
+    elif ctx.transport == "ipc":
+        par = (f"vocab-parallel x{world} (IPC transport: one process per rank, libfce collectives over CUDA IPC, "
+               f"{min(world, torch.cuda.device_count())} GPU(s))")
     else:
         par = (f"vocab-parallel x{world} (in-process local transport, {world} rank threads on "
                f"{args.local_gpus} GPU(s): the {world}-rank code path, not {world}-GPU throughput)")
@@ -501,7 +513,7 @@ def bench_rank(ctx, args):
         "metric": METRIC,
         "value": tokens_per_s,
         "unit": "tokens/s",
-        "n_gpus": world if ctx.transport == "nccl" else args.local_gpus,
+        "n_gpus": world if ctx.transport == "nccl" else min(world, torch.cuda.device_count()),
         "steps": args.steps,
         "warmup": max(args.warmup, 3),
         "ms_per_step": ms_step,
@@ -617,8 +629,9 @@ def main():
     ap.add_argument("--no-e2e-grads", action="store_true")
     ap.add_argument("--no-dropin", action="store_true", help="skip the C++ drop-in API end-to-end leg")
     ap.add_argument("--e2e-steps", type=int, default=16)
-    ap.add_argument("--transport", default="auto", choices=["auto", "nccl", "local"],
-                    help="N > 1 without torchrun: NCCL processes (needs N GPUs) or in-process local ranks")
+    ap.add_argument("--transport", default="auto", choices=["auto", "nccl", "ipc", "local"],
+                    help="N > 1 without torchrun: NCCL processes (needs N GPUs), IPC processes (libfce "
+                         "collectives, ranks may share GPUs) or in-process local ranks")
     ap.add_argument("--force-vp", action="store_true",
                     help="use the native vocab-parallel (NCCL) path even on one rank (testing)")
     args = ap.parse_args()
@@ -648,12 +661,13 @@ def main():
         ctx.close()
         print(json.dumps(line), flush=True)
         return 0
-    use_nccl = args.transport == "nccl" or (args.transport == "auto" and ngpu >= args.gpus)
-    if use_nccl:
-        # one process per GPU: re-launch under torch.distributed.run (rank 0 prints the line)
+    use_procs = args.transport in ("nccl", "ipc") or (args.transport == "auto" and ngpu >= args.gpus)
+    if use_procs:
+        # one process per rank: re-launch under torch.distributed.run (rank 0 prints the line)
+        env = dict(os.environ, FCE_BENCH_TRANSPORT="ipc" if args.transport == "ipc" else "nccl")
         cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
                "--master-addr=127.0.0.1", f"--master-port={_free_port()}", os.path.abspath(__file__)] + sys.argv[1:]
-        return subprocess.call(cmd)
+        return subprocess.call(cmd, env=env)
     # fewer GPUs than ranks: the N ranks as threads over the in-process transport
     from paper_2511_17599_b200 import vocab_parallel as vp
     devices = [r % max(ngpu, 1) for r in range(args.gpus)]

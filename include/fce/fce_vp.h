@@ -9,13 +9,16 @@
  * tensor_parallel, parallel_sim.hpp:55-57, exec.hpp:25-41) in an fce_problem
  * with v_offset / v_total set; H and targets are replicated.
  *
- * A communicator (fce_comm) has one of two transports:
+ * A communicator (fce_comm) has one of three transports:
  *   NCCL  (fce_comm_init)        one process per GPU, NCCL over NVLink /
  *                                NVSwitch — the production layout;
+ *   ipc   (fce_comm_init_ipc)    one process per rank on one node, the
+ *                                library's own collectives over CUDA IPC peer
+ *                                memory (no NCCL);
  *   local (fce_comm_init_local)  k ranks inside ONE process, each driven by
  *                                its own host thread, on any devices (several
- *                                may share one GPU); collectives are the
- *                                library's own peer-memory kernels.
+ *                                may share one GPU); the same peer-memory
+ *                                kernels.
  * Every collective entry point must be called by all ranks of the
  * communicator (for the local transport: concurrently, one thread per rank).
  * All device work is stream-ordered on the handle's stream.
@@ -34,13 +37,21 @@ typedef struct fce_comm_group_s* fce_comm_group;
 
 #define FCE_COMM_ID_BYTES 128
 
-enum { FCE_TRANSPORT_NCCL = 1, FCE_TRANSPORT_LOCAL = 2 };
+enum { FCE_TRANSPORT_NCCL = 1, FCE_TRANSPORT_LOCAL = 2, FCE_TRANSPORT_IPC = 3 };
 
 /* NCCL transport: rank 0 creates the id and ships it to the others (e.g. a
  * torch.distributed broadcast); every rank then calls fce_comm_init. */
 fce_status fce_comm_unique_id(uint8_t* out, size_t len);
 fce_status fce_comm_init(fce_comm* out, int device, int nranks, int rank, const uint8_t* id,
                          size_t len);
+/* IPC transport: one process per rank on one node, collectives by the
+ * library's own kernels over CUDA IPC peer memory (NVLink P2P; no NCCL).  Rank
+ * 0 makes the id (a rendezvous name, FCE_COMM_ID_BYTES), the caller ships it to
+ * the other processes, every rank calls fce_comm_init_ipc; ranks may share a
+ * GPU. */
+fce_status fce_comm_ipc_id(uint8_t* out, size_t len);
+fce_status fce_comm_init_ipc(fce_comm* out, int device, int nranks, int rank, const uint8_t* id,
+                             size_t len);
 /* Local transport: one group object shared by the k ranks of this process. */
 fce_status fce_comm_group_create(fce_comm_group* out, int nranks);
 fce_status fce_comm_group_destroy(fce_comm_group g); /* the group lives on until its last comm is destroyed */

@@ -82,7 +82,8 @@ EXPORTED_SYMBOLS = [
     "fce_forward_partial", "fce_merge_partials", "fce_backward", "fce_backward_ex", "fce_backward_dev",
     "fce_gemm_bf16", "fce_scale",
     "fce_generate_instance", "fce_f32_to_bf16",
-    "fce_comm_unique_id", "fce_comm_init", "fce_comm_group_create", "fce_comm_group_destroy",
+    "fce_comm_unique_id", "fce_comm_init", "fce_comm_ipc_id", "fce_comm_init_ipc",
+    "fce_comm_group_create", "fce_comm_group_destroy",
     "fce_comm_init_local", "fce_comm_destroy", "fce_comm_query", "fce_vp_last_error", "fce_comm_scratch_bytes",
     "fce_comm_all_gather", "fce_comm_all_reduce_f32", "fce_comm_reduce_scatter_f32",
     "fce_vp_forward", "fce_vp_backward", "fce_sp_gather", "fce_sp_scatter", "fce_dp_step",
@@ -126,6 +127,8 @@ def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
         "fce_f32_to_bf16": (I32, [P, P, I64, I64, I64, P, I64]),
         "fce_comm_unique_id": (I32, [P, ctypes.c_size_t]),
         "fce_comm_init": (I32, [ctypes.POINTER(P), I32, I32, I32, P, ctypes.c_size_t]),
+        "fce_comm_ipc_id": (I32, [P, ctypes.c_size_t]),
+        "fce_comm_init_ipc": (I32, [ctypes.POINTER(P), I32, I32, I32, P, ctypes.c_size_t]),
         "fce_comm_group_create": (I32, [ctypes.POINTER(P), I32]),
         "fce_comm_group_destroy": (I32, [P]),
         "fce_comm_init_local": (I32, [ctypes.POINTER(P), P, I32, I32]),

@@ -1,9 +1,16 @@
 // Communicator transports behind fce_comm (see fce_comm.h).
 #include <dlfcn.h>
+#include <fcntl.h>
 #include <nccl.h>
+#include <sys/mman.h>
+#include <sys/stat.h>
+#include <unistd.h>
 
 #include <algorithm>
+#include <atomic>
 #include <chrono>
+#include <random>
+#include <thread>
 #include <condition_variable>
 #include <cstdarg>
 #include <cstdio>
@@ -290,7 +297,313 @@ public:
     }
 };
 
+
+// ------------------------------------------------------------------ ipc
+// One process per rank on one node, collectives by the library's own kernels
+// over CUDA IPC peer memory (NVLink P2P between GPUs; plain HBM when ranks
+// share a GPU) — no NCCL.  Rendezvous through a POSIX shared-memory segment
+// named by the id: every rank publishes the IPC handles of its registered
+// staging buffer and of its phase events there, and the host barrier of a
+// phase is a generation counter in the segment.  Each collective stages its
+// input in the rank's registered buffer, so peers read it directly:
+//   all_gather      copy-in, phase, copy every peer's block out, phase
+//   all_reduce      copy-in, phase, sum slice r of every peer's input into
+//                   this rank's second region (rank order), phase, copy every
+//                   peer's reduced slice out, phase
+//   reduce_scatter  copy-in, phase, sum block r of every peer's input, phase
+struct IpcRankSlot {
+    int device;
+    int pid;
+    uint64_t buf_version;  // bumps whenever the rank re-registers its buffer
+    uint64_t buf_bytes;
+    cudaIpcMemHandle_t buf;
+    cudaIpcEventHandle_t ev[kPhases];
+};
+
+struct IpcShared {
+    uint32_t magic;
+    int nranks;
+    std::atomic<int> joined;
+    std::atomic<int> arrived;
+    std::atomic<uint64_t> gen;
+    std::atomic<int> aborted;
+    IpcRankSlot slot[kMaxLocalRanks];
+};
+static_assert(std::atomic<int>::is_always_lock_free && std::atomic<uint64_t>::is_always_lock_free,
+              "cross-process atomics must be lock free");
+constexpr uint32_t kIpcMagic = 0xFCE1BC01u;
+
+class IpcComm final : public Comm {
+public:
+    IpcShared* sh = nullptr;
+    std::string name;
+    cudaEvent_t ev[kPhases] = {nullptr, nullptr, nullptr};
+    cudaEvent_t peer_ev[kMaxLocalRanks][kPhases] = {};
+    char* buf = nullptr;  // registered staging buffer
+    size_t buf_bytes = 0;
+    uint64_t buf_version = 0;
+    char* peer_buf[kMaxLocalRanks] = {};
+    uint64_t peer_version[kMaxLocalRanks] = {};
+    double timeout_s = 600.0;
+
+    ~IpcComm() override {
+        for (int q = 0; q < nranks; ++q) {
+            if (q == rank) continue;
+            if (peer_buf[q]) cudaIpcCloseMemHandle(peer_buf[q]);
+            for (int ph = 0; ph < kPhases; ++ph)
+                if (peer_ev[q][ph]) cudaEventDestroy(peer_ev[q][ph]);
+        }
+        if (buf) cudaFree(buf);
+        for (cudaEvent_t e : ev)
+            if (e) cudaEventDestroy(e);
+        if (sh) munmap(sh, sizeof(IpcShared));
+    }
+    int transport() const override { return kTransportIpc; }
+
+    fce_status barrier() {
+        const uint64_t my = sh->gen.load();
+        if (sh->arrived.fetch_add(1) + 1 == nranks) {
+            sh->arrived.store(0);
+            sh->gen.fetch_add(1);
+            return FCE_OK;
+        }
+        const auto t0 = std::chrono::steady_clock::now();
+        int spins = 0;
+        while (sh->gen.load() == my) {
+            if (sh->aborted.load()) return comm_fail(FCE_NCCL_ERROR, "ipc communicator aborted by a peer rank");
+            if (++spins > 64) {
+                std::this_thread::sleep_for(std::chrono::microseconds(20));
+                if (std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count() > timeout_s) {
+                    sh->aborted.store(1);
+                    return comm_fail(FCE_NCCL_ERROR, "ipc collective timed out waiting for peer ranks");
+                }
+            }
+        }
+        return FCE_OK;
+    }
+
+    fce_status sync_phase(int phase, cudaStream_t s) {
+        FCE_COMM_CUDA(cudaEventRecord(ev[phase], s));
+        fce_status st = barrier();
+        if (st) return st;
+        for (int q = 0; q < nranks; ++q)
+            if (q != rank) FCE_COMM_CUDA(cudaStreamWaitEvent(s, peer_ev[q][phase], 0));
+        return FCE_OK;
+    }
+
+    // Grow the registered buffer (peers re-open it at their next collective).
+    fce_status ensure(size_t bytes, cudaStream_t s) {
+        if (bytes <= buf_bytes) return FCE_OK;
+        if (buf) {
+            // this stream already waited for every peer's reads of the old buffer
+            FCE_COMM_CUDA(cudaStreamSynchronize(s));
+            FCE_COMM_CUDA(cudaFree(buf));
+            buf = nullptr;
+        }
+        const size_t sz = std::max<size_t>(bytes, size_t(64) << 20);
+        FCE_COMM_CUDA(cudaMalloc(&buf, sz));
+        buf_bytes = sz;
+        IpcRankSlot& me = sh->slot[rank];
+        FCE_COMM_CUDA(cudaIpcGetMemHandle(&me.buf, buf));
+        me.buf_bytes = sz;
+        me.buf_version = ++buf_version;
+        return FCE_OK;
+    }
+
+    // After the first barrier of a collective: (re-)open peers' buffers that changed.
+    fce_status refresh_peers() {
+        for (int q = 0; q < nranks; ++q) {
+            if (q == rank) {
+                peer_buf[q] = buf;
+                continue;
+            }
+            const IpcRankSlot& p = sh->slot[q];
+            if (p.buf_version == peer_version[q] && peer_buf[q]) continue;
+            if (peer_buf[q]) FCE_COMM_CUDA(cudaIpcCloseMemHandle(peer_buf[q]));
+            void* ptr = nullptr;
+            FCE_COMM_CUDA(cudaIpcOpenMemHandle(&ptr, p.buf, cudaIpcMemLazyEnablePeerAccess));
+            peer_buf[q] = static_cast<char*>(ptr);
+            peer_version[q] = p.buf_version;
+        }
+        return FCE_OK;
+    }
+
+    fce_status all_gather(const void* send, void* recv, size_t bytes, cudaStream_t s) override {
+        NvtxRange nvtx_("ipc all_gather");
+        fce_status st = ensure(bytes, s);
+        if (st) return st;
+        if (bytes) FCE_COMM_CUDA(cudaMemcpyAsync(buf, send, bytes, cudaMemcpyDeviceToDevice, s));
+        if ((st = sync_phase(0, s)) || (st = refresh_peers())) return st;
+        for (int q = 0; q < nranks; ++q)
+            if (bytes)
+                FCE_COMM_CUDA(cudaMemcpyAsync(static_cast<char*>(recv) + static_cast<size_t>(q) * bytes, peer_buf[q],
+                                              bytes, cudaMemcpyDefault, s));
+        return sync_phase(1, s);
+    }
+
+    fce_status all_reduce_sum(const float* send, float* recv, size_t count, cudaStream_t s) override {
+        NvtxRange nvtx_("ipc all_reduce");
+        const size_t region = (count * sizeof(float) + 255) / 256 * 256;
+        fce_status st = ensure(2 * region, s);
+        if (st) return st;
+        if (count) FCE_COMM_CUDA(cudaMemcpyAsync(buf, send, count * sizeof(float), cudaMemcpyDeviceToDevice, s));
+        if ((st = sync_phase(0, s)) || (st = refresh_peers())) return st;
+        const size_t per = ((count + nranks - 1) / nranks + 3) / 4 * 4;
+        auto lo = [&](int q) { return std::min(count, static_cast<size_t>(q) * per); };
+        PeerPtrs src;
+        for (int q = 0; q < nranks; ++q) src.p[q] = reinterpret_cast<const float*>(peer_buf[q]) + lo(rank);
+        FCE_COMM_CUDA(launch_sum_peers(src, nranks, reinterpret_cast<float*>(buf + region) + lo(rank),
+                                       lo(rank + 1) - lo(rank), s));
+        if ((st = sync_phase(1, s))) return st;
+        for (int q = 0; q < nranks; ++q) {
+            if (lo(q + 1) == lo(q)) continue;
+            FCE_COMM_CUDA(cudaMemcpyAsync(recv + lo(q), reinterpret_cast<const float*>(peer_buf[q] + region) + lo(q),
+                                          (lo(q + 1) - lo(q)) * sizeof(float), cudaMemcpyDefault, s));
+        }
+        return sync_phase(2, s);
+    }
+
+    fce_status reduce_scatter_sum(const float* send, float* recv, size_t recv_count, cudaStream_t s) override {
+        NvtxRange nvtx_("ipc reduce_scatter");
+        const size_t bytes = recv_count * sizeof(float) * nranks;
+        fce_status st = ensure(bytes, s);
+        if (st) return st;
+        if (bytes) FCE_COMM_CUDA(cudaMemcpyAsync(buf, send, bytes, cudaMemcpyDeviceToDevice, s));
+        if ((st = sync_phase(0, s)) || (st = refresh_peers())) return st;
+        PeerPtrs src;
+        for (int q = 0; q < nranks; ++q)
+            src.p[q] = reinterpret_cast<const float*>(peer_buf[q]) + static_cast<size_t>(rank) * recv_count;
+        FCE_COMM_CUDA(launch_sum_peers(src, nranks, recv, recv_count, s));
+        return sync_phase(1, s);
+    }
+};
+
 }  // namespace
+
+fce_status ipc_unique_id(uint8_t* out, size_t len) {
+    if (!out || len < 64) return comm_fail(FCE_INVALID_ARGUMENT, "id buffer too small");
+    std::random_device rd;
+    char name[64];
+    snprintf(name, sizeof(name), "/fce_ipc_%d_%08x%08x", static_cast<int>(getpid()), rd(), rd());
+    std::memset(out, 0, len);
+    std::memcpy(out, name, std::strlen(name) + 1);
+    return FCE_OK;
+}
+
+fce_status make_ipc_comm(Comm** out, int device, int nranks, int rank, const uint8_t* id, size_t len) {
+    if (!out || !id || len < 64) return comm_fail(FCE_INVALID_ARGUMENT, "bad ipc id");
+    if (nranks < 1 || nranks > kMaxLocalRanks || rank < 0 || rank >= nranks)
+        return comm_fail(FCE_INVALID_LAYOUT, "ipc group size must be in [1, %d]", kMaxLocalRanks);
+    char name[64];
+    std::memcpy(name, id, 63);
+    name[63] = 0;
+    if (name[0] != '/') return comm_fail(FCE_INVALID_ARGUMENT, "not an ipc id (use fce_comm_ipc_id)");
+    FCE_COMM_CUDA(cudaSetDevice(device));
+    double timeout_s = 600.0;
+    if (const char* t = std::getenv("FCE_LOCAL_TIMEOUT_S")) timeout_s = std::atof(t) > 0 ? std::atof(t) : 600.0;
+    // rank 0 creates and sizes the segment; the others wait for it to appear
+    int fd = -1;
+    const auto t0 = std::chrono::steady_clock::now();
+    if (rank == 0) {
+        fd = shm_open(name, O_CREAT | O_RDWR, 0600);
+        if (fd < 0 || ftruncate(fd, sizeof(IpcShared)) != 0) {
+            if (fd >= 0) close(fd);
+            return comm_fail(FCE_NCCL_ERROR, "shm_open/ftruncate %s failed", name);
+        }
+    } else {
+        for (;;) {
+            fd = shm_open(name, O_RDWR, 0600);
+            if (fd >= 0) {
+                struct stat stt;
+                if (fstat(fd, &stt) == 0 && static_cast<size_t>(stt.st_size) >= sizeof(IpcShared)) break;
+                close(fd);
+                fd = -1;
+            }
+            if (std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count() > timeout_s)
+                return comm_fail(FCE_NCCL_ERROR, "ipc rendezvous %s not created by rank 0", name);
+            std::this_thread::sleep_for(std::chrono::milliseconds(2));
+        }
+    }
+    void* mem = mmap(nullptr, sizeof(IpcShared), PROT_READ | PROT_WRITE, MAP_SHARED, fd, 0);
+    close(fd);
+    if (mem == MAP_FAILED) return comm_fail(FCE_NCCL_ERROR, "mmap of %s failed", name);
+    IpcShared* sh = static_cast<IpcShared*>(mem);
+    if (rank == 0) {
+        sh->nranks = nranks;
+        sh->joined.store(0);
+        sh->arrived.store(0);
+        sh->gen.store(0);
+        sh->aborted.store(0);
+        std::atomic_thread_fence(std::memory_order_seq_cst);
+        reinterpret_cast<std::atomic<uint32_t>*>(&sh->magic)->store(kIpcMagic);
+    } else {
+        while (reinterpret_cast<std::atomic<uint32_t>*>(&sh->magic)->load() != kIpcMagic) {
+            if (std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count() > timeout_s) {
+                munmap(mem, sizeof(IpcShared));
+                return comm_fail(FCE_NCCL_ERROR, "ipc rendezvous %s never initialised", name);
+            }
+            std::this_thread::sleep_for(std::chrono::milliseconds(1));
+        }
+        if (sh->nranks != nranks) {
+            munmap(mem, sizeof(IpcShared));
+            return comm_fail(FCE_INVALID_LAYOUT, "ipc group has %d ranks, this rank expects %d", sh->nranks, nranks);
+        }
+    }
+    IpcComm* c = new IpcComm();
+    c->sh = sh;
+    c->name = name;
+    c->nranks = nranks;
+    c->rank = rank;
+    c->device = device;
+    c->timeout_s = timeout_s;
+    IpcRankSlot& me = sh->slot[rank];
+    me.device = device;
+    me.pid = static_cast<int>(getpid());
+    for (int ph = 0; ph < kPhases; ++ph) {
+        cudaError_t e = cudaEventCreateWithFlags(&c->ev[ph], cudaEventInterprocess | cudaEventDisableTiming);
+        if (e == cudaSuccess) e = cudaIpcGetEventHandle(&me.ev[ph], c->ev[ph]);
+        if (e != cudaSuccess) {
+            delete c;
+            return comm_fail(FCE_CUDA_ERROR, "ipc event: %s", cudaGetErrorString(e));
+        }
+    }
+    fce_status st = c->ensure(1, nullptr);
+    if (st) {
+        delete c;
+        return st;
+    }
+    // join: everyone's handles are published before anyone opens a peer's
+    sh->joined.fetch_add(1);
+    while (sh->joined.load() < nranks) {
+        if (std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count() > timeout_s) {
+            delete c;
+            return comm_fail(FCE_NCCL_ERROR, "ipc rendezvous: only %d of %d ranks joined", sh->joined.load(), nranks);
+        }
+        std::this_thread::sleep_for(std::chrono::microseconds(200));
+    }
+    for (int q = 0; q < nranks; ++q) {
+        if (q == rank) continue;
+        for (int ph = 0; ph < kPhases; ++ph) {
+            cudaError_t e = cudaIpcOpenEventHandle(&c->peer_ev[q][ph], sh->slot[q].ev[ph]);
+            if (e != cudaSuccess) {
+                delete c;
+                return comm_fail(FCE_CUDA_ERROR, "cudaIpcOpenEventHandle (rank %d): %s", q, cudaGetErrorString(e));
+            }
+        }
+    }
+    if ((st = c->refresh_peers())) {
+        delete c;
+        return st;
+    }
+    // every rank has opened the segment: the name can go (the mappings stay)
+    if ((st = c->barrier())) {
+        delete c;
+        return st;
+    }
+    if (rank == 0) shm_unlink(name);
+    *out = c;
+    return FCE_OK;
+}
 
 fce_status make_local_group(LocalGroup** out, int nranks) {
     if (!out) return comm_fail(FCE_INVALID_ARGUMENT, "null output");

@@ -16,6 +16,8 @@
 //          (reduce-scatter then all-gather, sums in rank order) — the
 //          peer-memory data path NVLink P2P gives a single-process multi-GPU
 //          job, and the way the k-rank code runs on a one-GPU box.
+//   ipc    one process per rank on one node, the same kernels over CUDA IPC
+//          mappings of each rank's registered staging buffer (no NCCL).
 #pragma once
 
 #include <cstddef>
@@ -26,7 +28,7 @@
 
 namespace fce {
 
-enum Transport : int { kTransportNccl = 1, kTransportLocal = 2 };
+enum Transport : int { kTransportNccl = 1, kTransportLocal = 2, kTransportIpc = 3 };
 
 class Comm {
 public:
@@ -44,6 +46,12 @@ public:
 // Transports (fce_comm.cpp).  Errors are reported through set_last_error.
 fce_status make_nccl_comm(Comm** out, int device, int nranks, int rank, const uint8_t* id, size_t len);
 fce_status nccl_unique_id(uint8_t* out, size_t len);
+
+// IPC transport: one process per rank on one node, the library's own
+// collectives over CUDA IPC peer memory; rendezvous through a POSIX
+// shared-memory segment named by the id (fce_comm.cpp).
+fce_status ipc_unique_id(uint8_t* out, size_t len);
+fce_status make_ipc_comm(Comm** out, int device, int nranks, int rank, const uint8_t* id, size_t len);
 
 struct LocalGroup;
 fce_status make_local_group(LocalGroup** out, int nranks);

@@ -184,6 +184,24 @@ fce_status fce_comm_init(fce_comm* out, int device, int nranks, int rank, const 
     return FCE_OK;
 }
 
+fce_status fce_comm_ipc_id(uint8_t* out, size_t len) { return fce::ipc_unique_id(out, len); }
+
+fce_status fce_comm_init_ipc(fce_comm* out, int device, int nranks, int rank, const uint8_t* id, size_t len) {
+    if (!out) return vp_fail(FCE_INVALID_ARGUMENT, "null output");
+    *out = nullptr;
+    fce::Comm* impl = nullptr;
+    fce_status s = fce::make_ipc_comm(&impl, device, nranks, rank, id, len);
+    if (s) return s;
+    fce_comm c = new fce_comm_s();
+    c->impl = impl;
+    if ((s = finish_comm_init(c))) {
+        fce_comm_destroy(c);
+        return s;
+    }
+    *out = c;
+    return FCE_OK;
+}
+
 fce_status fce_comm_group_create(fce_comm_group* out, int nranks) {
     if (!out) return vp_fail(FCE_INVALID_ARGUMENT, "null output");
     fce::LocalGroup* g = nullptr;

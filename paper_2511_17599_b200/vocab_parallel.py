@@ -54,13 +54,40 @@ class NativeComm:
         fce._check(lib.fce_comm_init(ctypes.byref(ptr), device, nranks, rank, buf, 128), vp=True)
         return cls(ptr, nranks, rank, device)
 
+    @staticmethod
+    def ipc_id() -> bytes:
+        """Rendezvous id of an IPC communicator (rank 0 makes it, ships it)."""
+        lib = fce.load_library()
+        buf = (ctypes.c_uint8 * 128)()
+        fce._check(lib.fce_comm_ipc_id(buf, 128), vp=True)
+        return bytes(buf)
+
+    @classmethod
+    def create_ipc(cls, nranks: int, rank: int, device: int, uid: bytes) -> "NativeComm":
+        """IPC transport: one process per rank, libfce's collectives over CUDA
+        IPC peer memory (no NCCL); ranks may share a GPU."""
+        lib = fce.load_library()
+        ptr = ctypes.c_void_p()
+        buf = (ctypes.c_uint8 * 128).from_buffer_copy(uid)
+        fce._check(lib.fce_comm_init_ipc(ctypes.byref(ptr), device, nranks, rank, buf, 128), vp=True)
+        return cls(ptr, nranks, rank, device)
+
+    @classmethod
+    def from_torch_distributed_ipc(cls, device: int, group=None) -> "NativeComm":
+        """IPC communicator over the ranks of a torch.distributed group (any backend)."""
+        import torch.distributed as dist
+        rank, world = dist.get_rank(group), dist.get_world_size(group)
+        obj = [cls.ipc_id() if rank == 0 else None]
+        dist.broadcast_object_list(obj, src=0, group=group)
+        return cls.create_ipc(world, rank, device, obj[0])
+
     @classmethod
     def create_local(cls, device: int = 0) -> "NativeComm":
         """A 1-rank NCCL communicator on `device`."""
         return cls.create(1, 0, device, cls.unique_id())
 
     def query(self):
-        """(nranks, rank, transport) with transport 1 = NCCL, 2 = local."""
+        """(nranks, rank, transport) with transport 1 = NCCL, 2 = local, 3 = ipc."""
         lib = fce.load_library()
         k, r, t = ctypes.c_int(), ctypes.c_int(), ctypes.c_int()
         fce._check(lib.fce_comm_query(self.ptr, ctypes.byref(k), ctypes.byref(r), ctypes.byref(t)), vp=True)

@@ -94,3 +94,23 @@ def test_cpu_baseline_fit_is_the_marginal_cost():
     import bench
     alpha, beta = bench._fit([(16, 10.0), (208, 14.8), (16, 10.2), (208, 15.0)])
     assert abs(beta - 0.025) < 1e-9 and abs(alpha - (10.1 - 0.025 * 16)) < 1e-9
+
+
+@pytest.mark.gpu
+def test_gpu_arm_ipc_transport_processes(cuda):
+    """`bench.py --gpus 2 --transport ipc`: two processes (torch.distributed.run,
+    gloo for the launcher's barrier) sharing this GPU, vocab-parallel over
+    libfce's own IPC collectives; one JSON line, the single-GPU loss."""
+    r = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--gpus", "2", "--transport", "ipc",
+                        "--config", "small", "--steps", "2", "--warmup", "3", "--e2e-steps", "2", "--no-cpu-baseline",
+                        "--no-e2e-grads"], cwd=ROOT, capture_output=True, text=True, timeout=900)
+    assert r.returncode == 0, r.stderr[-3000:]
+    lines = _json_lines(r.stdout)
+    assert len(lines) == 1
+    d = lines[0]
+    assert d["config"]["ranks"] == 2 and "IPC transport" in d["config"]["parallelism"]
+    r1 = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--config", "small", "--steps", "2",
+                         "--warmup", "3", "--e2e-steps", "2", "--no-cpu-baseline", "--no-e2e-grads", "--no-dropin"],
+                        cwd=ROOT, capture_output=True, text=True, timeout=600)
+    d1 = _json_lines(r1.stdout)[0]
+    assert abs(d["loss"] - d1["loss"]) <= 1e-5 * abs(d1["loss"])

@@ -10,6 +10,8 @@ tp_backward / sp_to_tp_gather / dp_step (parallel_sim.hpp:165-378) on the same
 bf16-grid inputs.  Tolerances as tests/test_parity_gpu.py: loss / lse 1e-3
 relative, dH / dW 1e-2 relative max-norm, found flags and ignored rows exact.
 """
+import os
+
 import numpy as np
 import pytest
 import torch
@@ -328,3 +330,45 @@ def test_random_multirank_cases(cuda, case):
             assert abs(out.loss.item() - lred) <= LOSS_RTOL * max(1.0, abs(lred))
         assert relmax(dh.cpu().numpy(), dH) < GRAD_RTOL
     assert relmax(np.concatenate([x[2].cpu().numpy() for x in res]), dW) < GRAD_RTOL
+
+
+@pytest.mark.parametrize("k,ign,chunks", [(2, None, 0), (3, -100, 0), (4, None, 2)])
+def test_ipc_transport_multiprocess(cuda, tmp_path, k, ign, chunks):
+    """k separate processes (all on this GPU) over the IPC transport: CUDA IPC
+    mappings of each rank's registered buffer, cross-process events and a
+    shared-memory barrier — the one-process-per-rank data path without NCCL.
+    Every rank's loss / stats / dH and the concatenated dW shards against the
+    oracle; the raw collectives bit-exact against rank-ordered sums."""
+    import subprocess
+    import sys
+    n, d, v = 600 if chunks else 300, 136, 2500
+    H, W, Y = ob.make_instance(n, d, v, 70 + k, -100, 0.2 if ign is not None else 0.0)
+    rng = np.random.default_rng(k)
+    x = rng.standard_normal((k, 777)).astype(np.float32)
+    inp = tmp_path / "in.npz"
+    np.savez(inp, H=H, W=W, Y=Y, ign=-100, has_ign=int(ign is not None), x=x, chunks=chunks)
+    uid = vp.NativeComm.ipc_id().hex()
+    helper = os.path.join(os.path.dirname(os.path.abspath(__file__)), "helpers", "ipc_rank.py")
+    env = dict(os.environ, FCE_LOCAL_TIMEOUT_S="300")
+    procs = [subprocess.Popen([sys.executable, helper, str(r), str(k), uid, str(inp), str(tmp_path / f"out{r}.npz")],
+                              env=env, stdout=subprocess.PIPE, stderr=subprocess.STDOUT, text=True)
+             for r in range(k)]
+    logs = [p.communicate(timeout=600)[0] for p in procs]
+    for p, log in zip(procs, logs):
+        assert p.returncode == 0, log[-3000:]
+    outs = [np.load(tmp_path / f"out{r}.npz") for r in range(k)]
+    st, rows, lred = ob.forward(H, W, Y, "mean", ign)
+    dH, dW = ob.backward(H, W, Y, st, "mean", 1.0, ign)
+    ref_s = x[0].copy()
+    for r in range(1, k):
+        ref_s = (ref_s + x[r]).astype(np.float32)
+    tot = sum(range(1, k + 1))
+    for r, o in enumerate(outs):
+        np.testing.assert_array_equal(o["found"], st["found"])
+        assert abs(float(o["loss"]) - lred) <= LOSS_RTOL * max(1.0, abs(lred))
+        assert relmax(o["dh"], dH) < GRAD_RTOL
+        np.testing.assert_array_equal(o["dh"], outs[0]["dh"])
+        np.testing.assert_array_equal(o["s"], ref_s)
+        np.testing.assert_array_equal(o["g"], np.repeat(np.arange(k, dtype=np.float32)[:, None], 5, 1))
+        np.testing.assert_array_equal(o["rs"], np.arange(r * 9, r * 9 + 9, dtype=np.float32) * tot)
+    assert relmax(np.concatenate([o["dw"] for o in outs]), dW) < GRAD_RTOL
