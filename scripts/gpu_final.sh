@@ -1,0 +1,5 @@
+# Final captures of the round's sources: full GPU suite, per-config bench + ncu.
+set -x
+timeout 1800 python -m pytest tests -x -q -m gpu > gpurun_out/final_tests.log 2>&1; echo "rc=$?" >> gpurun_out/final_tests.log
+TAG=r02f bash scripts/gpu_configs.sh
+tail -n 3 gpurun_out/final_tests.log
