@@ -101,6 +101,18 @@ fce_status fce_sp_gather(fce_handle h, fce_comm c, const void* shard, int64_t sh
 fce_status fce_sp_scatter(fce_handle h, fce_comm c, const float* dh_partial, int64_t n_total, int64_t lddh,
                           int64_t d, float* dh_shard, int64_t shard_rows, int64_t ld_shard);
 
+/* tp_backward followed by the sequence-parallel reduce-scatter of dH, as one
+ * call: rank r receives the summed dH rows of its position shard (fp32
+ * [shard_rows, ld_shard]; shards consecutive in rank order) and its local dW
+ * shard.  With a peer-memory transport (local, ipc) and no ignore_index the
+ * reduction happens inside the backward kernel: every dH tile is
+ * TMA-reduce-added into the accumulator of the rank owning its rows while the
+ * kernel runs (no separate reduce-scatter pass; sums across ranks in arrival
+ * order).  Otherwise: local dH, then fce_sp_scatter. */
+fce_status fce_sp_vp_backward(fce_handle h, fce_comm c, const fce_problem* p, fce_stats merged, int reduction,
+                              float upstream_scalar, const float* upstream_rows, float* dh_shard, int64_t shard_rows,
+                              int64_t ld_shard, float* dweight_shard, int64_t lddw);
+
 /* dp_step (parallel_sim.hpp:334-378): every rank runs the fused forward and
  * backward on its micro-batch (p), then loss and dW are averaged over the
  * ranks (all-reduce / nranks); dH stays rank-local (may be NULL).  Micro-

@@ -68,6 +68,7 @@ struct fce_handle_s {
     int64_t vp_overlap_chunks = 0;  // fce_vp_backward: row chunks whose dH all-reduce overlaps the kernel (0: off)
     int64_t vp_reserve_sms = 8;     // ... and the SMs the kernel leaves to the collectives
     int64_t comm_trace_ptr = 0;     // dev only: globaltimer stamps of the overlapped collectives
+    int64_t vp_fused_dh = 0;        // fce_vp_backward: reduce dH inside the kernel over peer memory
     // last persistent backward launch: where each row chunk's dH completion is counted
     struct LastBwd {
         bool valid = false;
@@ -75,6 +76,12 @@ struct fce_handle_s {
         int64_t row_chunk = 0, n_rc = 0, bands = 0, n_dh = 0;
     } last_bwd;
     cudaEvent_t ctr_reset_ev = nullptr;  // when set: recorded right after the counter reset
+    // when k > 0: the next persistent backward reduces dH into these owners' accumulators
+    struct DhPeers {
+        int k = 0;
+        float* ptr[kMaxDhPeers] = {};
+        int block0[kMaxDhPeers + 1] = {};
+    } dh_peers;
     // compaction buffers (grow-only, separate from ws so both can be live)
     void* cws = nullptr;
     size_t cws_size = 0;
@@ -104,6 +111,7 @@ cudaStream_t handle_stream(fce_handle h) { return h ? h->stream : nullptr; }
 int64_t handle_vp_overlap_chunks(fce_handle h) { return h ? h->vp_overlap_chunks : 0; }
 int64_t handle_vp_reserve_sms(fce_handle h) { return h ? h->vp_reserve_sms : 0; }
 int handle_device(fce_handle h) { return h ? h->device : 0; }
+int64_t handle_vp_fused_dh(fce_handle h) { return h ? h->vp_fused_dh : 0; }
 unsigned long long* handle_comm_trace(fce_handle h) {
     return h ? reinterpret_cast<unsigned long long*>(h->comm_trace_ptr) : nullptr;
 }
@@ -475,6 +483,8 @@ fce_status run_backward_persistent(fce_handle h, const fce_problem* p, const flo
     bp.v_offset = p->v_offset;
     bp.ignore_index = p->ignore_index;
     bp.counters = d_ctr;
+    bp.dh_peers = dhidden ? h->dh_peers.k : 0;
+    for (int q = 0; q <= kMaxDhPeers; ++q) bp.peer_block0[q] = h->dh_peers.block0[q];
     bp.targets = p->targets;
     bp.lse = lse;
     bp.gamma = gamma;
@@ -524,6 +534,14 @@ fce_status run_backward_persistent(fce_handle h, const fce_problem* p, const flo
     }
     if (dw_bf16 && !(bp.tma_epi & 2))
         return fail(FCE_CUDA_ERROR, "bf16 dW needs the TMA epilogue (16-byte aligned rows)");
+    if (bp.dh_peers > 0) {
+        // every dH tile is reduce-added into its owner rank's accumulator
+        bool ok = (bp.tma_epi & 2) != 0;
+        for (int q = 0; ok && q < bp.dh_peers; ++q)
+            ok = encode_map_2d(&maps.dh_peer[q], h->dh_peers.ptr[q], p->d, p->n, lddh * 4, 32, 128, true);
+        if (!ok) return fail(FCE_CUDA_ERROR, "peer dH reduction needs the TMA epilogue and aligned accumulators");
+        bp.accumulate_dh = 1;
+    }
     TimedRegion tr(h);
     const int grid = static_cast<int>(std::max<int64_t>(2, h->sms - h->bwd_reserve_sms));
     cudaError_t e = launch_bwd_persistent(bp, maps, grid, h->stream);
@@ -663,6 +681,8 @@ fce_status fce_set_option(fce_handle h, const char* key, int64_t value) {
     } else if (!std::strcmp(key, "vp_overlap_chunks")) {
         if (value == 1 || value > 64) return fail(FCE_INVALID_ARGUMENT, "vp_overlap_chunks must be 0 or in [2, 64]");
         h->vp_overlap_chunks = value;
+    } else if (!std::strcmp(key, "vp_fused_dh")) {
+        h->vp_fused_dh = value ? 1 : 0;
     } else if (!std::strcmp(key, "comm_trace_ptr")) {
         h->comm_trace_ptr = value;
     } else if (!std::strcmp(key, "vp_reserve_sms")) {
@@ -1295,6 +1315,23 @@ fce_status backward_for_overlap(fce_handle h, const fce_problem* p, fce_stats st
         done->push_back(d);
     }
     return FCE_OK;
+}
+
+fce_status backward_dh_peers(fce_handle h, const fce_problem* p, fce_stats stats, int reduction,
+                             float upstream_scalar, const float* upstream_rows, float* const* peer_dh, int k,
+                             const int* block0, float* dweight, int64_t lddw) {
+    fce_status s = check_handle(h);
+    if (s) return s;
+    if (k < 1 || k > kMaxDhPeers) return fail(FCE_INVALID_LAYOUT, "peer dH reduction supports 1..%d ranks", kMaxDhPeers);
+    if (!h->bwd_persistent || p->has_ignore)
+        return fail(FCE_INVALID_ARGUMENT, "peer dH reduction needs the persistent backward and no ignore_index");
+    h->dh_peers.k = k;
+    for (int q = 0; q < k; ++q) h->dh_peers.ptr[q] = peer_dh[q];
+    for (int q = 0; q <= k; ++q) h->dh_peers.block0[q] = block0[q];
+    s = backward_impl(h, p, stats, reduction, upstream_scalar, nullptr, upstream_rows, peer_dh[0], p->d, FCE_DTYPE_F32,
+                      dweight, lddw, FCE_DTYPE_F32, 1);
+    h->dh_peers.k = 0;
+    return s;
 }
 
 }  // namespace fce

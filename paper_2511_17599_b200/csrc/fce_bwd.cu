@@ -591,6 +591,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(128 + 32 * kEpiWarps
                         const bool accumulate = is_dh ? (un.gl > 0 || p.accumulate_dh) : (un.row_idx > 0);
                         const CUtensorMap* om = is_dh ? &maps.dh_st : &maps.dw_st;
                         const int orow = (is_dh ? un.r0 : un.vb) + un.m_blk * kPM + static_cast<int>(rank) * 128;
+                        if (is_dh && p.dh_peers > 0) {
+                            // reduce into the accumulator of the rank owning this 128-row block
+                            const int blk = orow >> 7;
+                            int q = 0;
+                            while (q + 1 < p.dh_peers && blk >= p.peer_block0[q + 1]) ++q;
+                            om = &maps.dh_peer[q];
+                        }
                         // debug: bit 5 discards dH and dW writes, bit 6 only dH, bit 7 only dW
                         const bool discard = ((p.unit_mask >> 5) & 1) || ((p.unit_mask >> (is_dh ? 6 : 7)) & 1);
 #pragma unroll 1

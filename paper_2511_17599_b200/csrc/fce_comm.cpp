@@ -116,6 +116,13 @@ public:
 
 }  // namespace
 
+fce_status Comm::sym_buffers(size_t, cudaStream_t, void**) {
+    return comm_fail(FCE_INVALID_ARGUMENT, "this transport has no peer memory (use the local or ipc transport)");
+}
+fce_status Comm::fence(cudaStream_t) {
+    return comm_fail(FCE_INVALID_ARGUMENT, "this transport has no stream fence");
+}
+
 fce_status nccl_unique_id(uint8_t* out, size_t len) {
     if (!out || len < sizeof(ncclUniqueId)) return comm_fail(FCE_INVALID_ARGUMENT, "id buffer too small");
     NcclApi& api = nccl();
@@ -166,6 +173,7 @@ struct LocalGroup {
     std::vector<const void*> send; // published buffers of the current collective
     std::vector<void*> recv;
     std::vector<cudaEvent_t> ev;   // [phase][rank] published events
+    std::vector<void*> sym;        // per rank: symmetric peer-memory region
     double timeout_s = 600.0;
 };
 
@@ -178,11 +186,40 @@ public:
     LocalGroup* g = nullptr;
     cudaEvent_t ev[kPhases] = {nullptr, nullptr, nullptr};
     bool peers_ready = false;
+    void* sym = nullptr;
+    size_t sym_bytes = 0;
 
     ~LocalComm() override {
         for (cudaEvent_t e : ev)
             if (e) cudaEventDestroy(e);
+        if (sym) cudaFree(sym);
         release_local_group(g);
+    }
+    bool has_peer_memory() const override { return true; }
+
+    fce_status fence(cudaStream_t s) override { return sync_phase(0, s); }
+
+    fce_status sym_buffers(size_t bytes, cudaStream_t s, void** ptrs) override {
+        if (bytes > sym_bytes) {
+            if (sym) {
+                // the last use ended with a fence: peers no longer read it
+                FCE_COMM_CUDA(cudaStreamSynchronize(s));
+                FCE_COMM_CUDA(cudaFree(sym));
+                sym = nullptr;
+            }
+            FCE_COMM_CUDA(cudaMalloc(&sym, bytes));
+            sym_bytes = bytes;
+        }
+        {
+            std::lock_guard<std::mutex> lk(g->mu);
+            g->sym[rank] = sym;
+        }
+        fce_status st = sync_phase(0, s);
+        if (st) return st;
+        if ((st = enable_peers())) return st;
+        std::lock_guard<std::mutex> lk(g->mu);
+        for (int q = 0; q < nranks; ++q) ptrs[q] = g->sym[q];
+        return FCE_OK;
     }
     int transport() const override { return kTransportLocal; }
 
@@ -318,6 +355,9 @@ struct IpcRankSlot {
     uint64_t buf_bytes;
     cudaIpcMemHandle_t buf;
     cudaIpcEventHandle_t ev[kPhases];
+    uint64_t sym_version;  // symmetric peer-memory region (fused dH reduction)
+    uint64_t sym_bytes;
+    cudaIpcMemHandle_t sym;
 };
 
 struct IpcShared {
@@ -344,21 +384,65 @@ public:
     uint64_t buf_version = 0;
     char* peer_buf[kMaxLocalRanks] = {};
     uint64_t peer_version[kMaxLocalRanks] = {};
+    char* sym = nullptr;
+    size_t sym_bytes = 0;
+    uint64_t sym_version = 0;
+    char* peer_sym[kMaxLocalRanks] = {};
+    uint64_t peer_sym_version[kMaxLocalRanks] = {};
     double timeout_s = 600.0;
 
     ~IpcComm() override {
         for (int q = 0; q < nranks; ++q) {
             if (q == rank) continue;
             if (peer_buf[q]) cudaIpcCloseMemHandle(peer_buf[q]);
+            if (peer_sym[q]) cudaIpcCloseMemHandle(peer_sym[q]);
             for (int ph = 0; ph < kPhases; ++ph)
                 if (peer_ev[q][ph]) cudaEventDestroy(peer_ev[q][ph]);
         }
         if (buf) cudaFree(buf);
+        if (sym) cudaFree(sym);
         for (cudaEvent_t e : ev)
             if (e) cudaEventDestroy(e);
         if (sh) munmap(sh, sizeof(IpcShared));
     }
     int transport() const override { return kTransportIpc; }
+    bool has_peer_memory() const override { return true; }
+
+    fce_status fence(cudaStream_t s) override { return sync_phase(0, s); }
+
+    fce_status sym_buffers(size_t bytes, cudaStream_t s, void** ptrs) override {
+        IpcRankSlot& me = sh->slot[rank];
+        if (bytes > sym_bytes) {
+            if (sym) {
+                FCE_COMM_CUDA(cudaStreamSynchronize(s));
+                FCE_COMM_CUDA(cudaFree(sym));
+                sym = nullptr;
+            }
+            FCE_COMM_CUDA(cudaMalloc(&sym, bytes));
+            sym_bytes = bytes;
+            FCE_COMM_CUDA(cudaIpcGetMemHandle(&me.sym, sym));
+            me.sym_bytes = bytes;
+            me.sym_version = ++sym_version;
+        }
+        fce_status st = sync_phase(0, s);
+        if (st) return st;
+        for (int q = 0; q < nranks; ++q) {
+            if (q == rank) {
+                ptrs[q] = sym;
+                continue;
+            }
+            const IpcRankSlot& p = sh->slot[q];
+            if (p.sym_version != peer_sym_version[q] || !peer_sym[q]) {
+                if (peer_sym[q]) FCE_COMM_CUDA(cudaIpcCloseMemHandle(peer_sym[q]));
+                void* ptr = nullptr;
+                FCE_COMM_CUDA(cudaIpcOpenMemHandle(&ptr, p.sym, cudaIpcMemLazyEnablePeerAccess));
+                peer_sym[q] = static_cast<char*>(ptr);
+                peer_sym_version[q] = p.sym_version;
+            }
+            ptrs[q] = peer_sym[q];
+        }
+        return FCE_OK;
+    }
 
     fce_status barrier() {
         const uint64_t my = sh->gen.load();
@@ -615,6 +699,7 @@ fce_status make_local_group(LocalGroup** out, int nranks) {
     g->send.assign(nranks, nullptr);
     g->recv.assign(nranks, nullptr);
     g->ev.assign(kPhases * nranks, nullptr);
+    g->sym.assign(nranks, nullptr);
     if (const char* t = std::getenv("FCE_LOCAL_TIMEOUT_S")) g->timeout_s = std::atof(t) > 0 ? std::atof(t) : 600.0;
     *out = g;
     return FCE_OK;

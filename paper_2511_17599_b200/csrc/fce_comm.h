@@ -38,6 +38,14 @@ public:
     virtual fce_status all_reduce_sum(const float* send, float* recv, size_t count, cudaStream_t s) = 0;
     virtual fce_status reduce_scatter_sum(const float* send, float* recv, size_t recv_count,
                                           cudaStream_t s) = 0;
+    // Peer-memory transports only (local, ipc).  Collective: every rank's
+    // symmetric region of >= bytes, as pointers usable by this rank's kernels
+    // (its own first at ptrs[rank]); the regions persist between calls.
+    virtual bool has_peer_memory() const { return false; }
+    virtual fce_status sym_buffers(size_t bytes, cudaStream_t s, void** ptrs);
+    // Collective stream fence: work queued on every rank's stream before it
+    // completes before work queued after it on any rank's stream.
+    virtual fce_status fence(cudaStream_t s);
     int nranks = 1;
     int rank = 0;
     int device = 0;

@@ -36,6 +36,9 @@ constexpr int kSmemBytes = kStages * (kStageBytesA + kStageBytesB) + 1024 /*alig
 
 enum EpilogueMode : int { kEpiForward = 0, kEpiGrad = 1, kEpiGemm = 2 };
 
+// Ranks whose dH accumulators one persistent backward can reduce into directly.
+constexpr int kMaxDhPeers = 8;
+
 // One GEMM problem C[M,N] (+)= A[M,K] * B[N,K]^T for the generic epilogue.
 struct GemmProblem {
     int m, n, k_blocks;
@@ -100,6 +103,12 @@ struct BwdParams {
     const unsigned long long* n_valid;  // device count of live rows (compacted problems; NULL: n)
     int l2_hints;            // bit0: evict_first on dH/dW writes, bit1: evict_last on G loads,
                              // bit2: evict_last on G stores, bit3: evict_first on H loads (dW)
+    // dH reduced across ranks inside the kernel (vocab-parallel over peer
+    // memory): every dH tile is TMA-reduce-added into the symmetric accumulator
+    // of the rank owning its 128-row block; owners hold blocks
+    // [peer_block0[q], peer_block0[q + 1]) (0 peers: local dH as usual)
+    int dh_peers;
+    int peer_block0[kMaxDhPeers + 1];
     int64_t nc_max, ldg, ldr, d, lddh, lddw, v_offset, ignore_index;  // ldg = band, ldr = kg * band
     unsigned* counters;      // [0] scheduler, 4 per chunk, then mb_max per chunk
     unsigned long long* trace;  // dev only: [units][8] = MMA start, MMA end, epilogue end, smid,
@@ -115,6 +124,7 @@ struct BwdParams {
 struct BwdMaps {
     CUtensorMap h_k, w_k, g_k, w_mn, g_mn, h_mn;
     CUtensorMap g_st, dh_st, dw_st;  // epilogue TMA stores / reduce-adds (tma_epi)
+    CUtensorMap dh_peer[kMaxDhPeers];  // owners' dH accumulators (dh_peers > 0)
 };
 
 cudaError_t launch_fwd_pair(const TileParams& p, const TensorMaps& maps, int sms, cudaStream_t stream);
@@ -152,6 +162,14 @@ fce_status backward_for_overlap(fce_handle h, const fce_problem* p, fce_stats st
                                 float upstream_scalar, const float* upstream_rows, float* dhidden, int64_t lddh,
                                 float* dweight, int64_t lddw, int64_t row_chunk, int reserve_sms,
                                 cudaEvent_t counters_reset, std::vector<DhChunkDone>* done);
+// fce_backward whose dH tiles are reduce-added (TMA, fp32) straight into the
+// owning rank's dH accumulator: peer_dh[q] are the k ranks' [n, d]
+// accumulators as mapped in this process (peer memory), rank q owning the
+// 128-row blocks [block0[q], block0[q + 1]).  The accumulators must be zeroed
+// (owned rows) before any rank's kernel starts; dW stays local (fce_api.cpp).
+fce_status backward_dh_peers(fce_handle h, const fce_problem* p, fce_stats stats, int reduction,
+                             float upstream_scalar, const float* upstream_rows, float* const* peer_dh, int k,
+                             const int* block0, float* dweight, int64_t lddw);
 // Stream-ordered wait until *counter >= target (cuStreamWaitValue32, or a
 // one-thread spin kernel where stream memory operations are unavailable).
 cudaError_t stream_wait_geq(cudaStream_t s, const unsigned* counter, unsigned target);
@@ -162,6 +180,8 @@ int handle_device(fce_handle h);
 // Options "vp_overlap_chunks" / "vp_reserve_sms" of the handle (fce_vp_backward).
 int64_t handle_vp_overlap_chunks(fce_handle h);
 int64_t handle_vp_reserve_sms(fce_handle h);
+// Option "vp_fused_dh": fce_vp_backward reduces dH inside the kernel (peer memory).
+int64_t handle_vp_fused_dh(fce_handle h);
 // Option "comm_trace_ptr" (dev): u64 slots for globaltimer stamps, 2 per chunk.
 unsigned long long* handle_comm_trace(fce_handle h);
 cudaError_t launch_stamp(cudaStream_t s, unsigned long long* slot);

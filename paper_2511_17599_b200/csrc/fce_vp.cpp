@@ -159,6 +159,52 @@ fce_status vp_backward_overlapped(fce_handle h, fce_comm c, const fce_problem* p
     return FCE_OK;
 }
 
+// dH reduced inside the backward over peer memory (local / ipc transports):
+// every rank's dH tiles are TMA-reduce-added straight into the symmetric
+// accumulator of the rank owning their 128-row block, while the kernel runs —
+// the dH reduce-scatter costs no separate pass.  owner q holds the blocks
+// [block0[q], block0[q + 1]).  Then each rank copies out the rows it needs:
+// every owner's rows (tp_backward semantics: the full dH) or the rows of its own
+// position shard [sp_lo, sp_hi) (sequence-parallel semantics).
+fce_status vp_backward_fused(fce_handle h, fce_comm c, const fce_problem* p, fce_stats merged, int reduction,
+                             float upstream_scalar, const float* upstream_rows, const int* block0, float* out,
+                             int64_t ld_out, int64_t out_row0, int64_t out_rows, float* dweight_shard,
+                             int64_t lddw) {
+    const int k = c->impl->nranks, r = c->impl->rank;
+    cudaStream_t stream = fce::handle_stream(h);
+    const int64_t n = p->n, d = p->d;
+    void* sym[fce::kMaxDhPeers];
+    fce_status s = c->impl->sym_buffers(sizeof(float) * static_cast<size_t>(n) * d, stream, sym);
+    if (s) return s;
+    auto own_lo = [&](int q) { return std::min<int64_t>(n, int64_t(block0[q]) * 128); };
+    // zero the rows this rank owns, then no rank's kernel starts before every
+    // owner has zeroed
+    if (own_lo(r + 1) > own_lo(r))
+        VP_CUDA(cudaMemsetAsync(static_cast<float*>(sym[r]) + own_lo(r) * d, 0,
+                                sizeof(float) * (own_lo(r + 1) - own_lo(r)) * d, stream));
+    if ((s = c->impl->fence(stream))) return s;
+    float* peers[fce::kMaxDhPeers];
+    for (int q = 0; q < k; ++q) peers[q] = static_cast<float*>(sym[q]);
+    if ((s = fce::backward_dh_peers(h, p, merged, reduction, upstream_scalar, upstream_rows, peers, k, block0,
+                                    dweight_shard, lddw)))
+        return s;
+    // every rank's reduce-adds have landed
+    if ((s = c->impl->fence(stream))) return s;
+    for (int q = 0; q < k; ++q) {
+        const int64_t lo = std::max(own_lo(q), out_row0), hi = std::min(own_lo(q + 1), out_row0 + out_rows);
+        if (hi <= lo) continue;
+        VP_CUDA(cudaMemcpy2DAsync(out + (lo - out_row0) * ld_out, sizeof(float) * ld_out, peers[q] + lo * d,
+                                  sizeof(float) * d, sizeof(float) * d, hi - lo, cudaMemcpyDefault, stream));
+    }
+    // peers are done reading this rank's accumulator before it is reused
+    return c->impl->fence(stream);
+}
+
+bool fused_dh_possible(fce_comm c, const fce_problem* p) {
+    return c->impl->has_peer_memory() && c->impl->nranks <= fce::kMaxDhPeers && !p->has_ignore &&
+           (p->d * 4) % 16 == 0;
+}
+
 }  // namespace
 
 extern "C" {
@@ -318,6 +364,15 @@ fce_status fce_vp_backward(fce_handle h, fce_comm c, const fce_problem* p, fce_s
                             lddw, 0);
     if (lddh < p->d) return vp_fail(FCE_DIMENSION_MISMATCH, "lddh < d");
     cudaStream_t stream = fce::handle_stream(h);
+    if (fce::handle_vp_fused_dh(h) && fused_dh_possible(c, p)) {
+        // owners: ceil-first partition of the 128-row blocks over the ranks
+        const int k = c->impl->nranks;
+        const int64_t nb = (p->n + 127) / 128;
+        int block0[fce::kMaxDhPeers + 1];
+        for (int q = 0; q <= k; ++q) block0[q] = static_cast<int>((nb / k) * q + std::min<int64_t>(q, nb % k));
+        return vp_backward_fused(h, c, p, merged, reduction, upstream_scalar, upstream_rows, block0, dhidden, lddh,
+                                 0, p->n, dweight_shard, lddw);
+    }
     const int64_t chunks = fce::handle_vp_overlap_chunks(h);
     if (chunks > 1 && lddh == p->d && !p->has_ignore && p->n >= 256 * chunks)
         return vp_backward_overlapped(h, c, p, merged, reduction, upstream_scalar, upstream_rows, dhidden,
@@ -416,6 +471,53 @@ fce_status fce_sp_scatter(fce_handle h, fce_comm c, const float* dh_partial, int
     }
     if ((s = c->impl->reduce_scatter_sum(send, recv, blk_elems, stream))) return s;
     return copy_rows(dh_shard, sizeof(float) * ld_shard, recv, row_b, row_b, all[4 * r], stream);
+}
+
+fce_status fce_sp_vp_backward(fce_handle h, fce_comm c, const fce_problem* p, fce_stats merged, int reduction,
+                              float upstream_scalar, const float* upstream_rows, float* dh_shard, int64_t shard_rows,
+                              int64_t ld_shard, float* dweight_shard, int64_t lddw) {
+    fce::NvtxRange nvtx_("fce_sp_vp_backward");
+    fce_status s = check_args(h, c);
+    if (s) return s;
+    if (!p) return vp_fail(FCE_INVALID_ARGUMENT, "null problem");
+    if (shard_rows < 0 || (shard_rows > 0 && (!dh_shard || ld_shard < p->d)))
+        return vp_fail(FCE_INVALID_ARGUMENT, "bad dH shard buffer");
+    const int k = c->impl->nranks, r = c->impl->rank;
+    cudaStream_t stream = fce::handle_stream(h);
+    // the ranks' position shards (consecutive in rank order)
+    std::vector<int64_t> all;
+    const int64_t mine[1] = {shard_rows};
+    if ((s = exchange(c, stream, mine, 1, &all))) return s;
+    int64_t total = 0, lo = 0;
+    std::vector<int64_t> starts(k + 1, 0);
+    for (int q = 0; q < k; ++q) {
+        starts[q] = total;
+        if (q == r) lo = total;
+        total += all[4 * q];
+    }
+    starts[k] = total;
+    if (total != p->n)
+        return vp_fail(FCE_DIMENSION_MISMATCH, "shard rows add up to %lld, not N = %lld", (long long)total,
+                       (long long)p->n);
+    if (fused_dh_possible(c, p)) {
+        // block b belongs to the rank whose shard holds its first row
+        int block0[fce::kMaxDhPeers + 1];
+        const int64_t nb = (p->n + 127) / 128;
+        for (int q = 0; q < k; ++q) block0[q] = static_cast<int>(std::min<int64_t>(nb, (starts[q] + 127) / 128));
+        block0[k] = static_cast<int>(nb);
+        for (int q = k - 1; q >= 0; --q) block0[q] = std::min(block0[q], block0[q + 1]);
+        return vp_backward_fused(h, c, p, merged, reduction, upstream_scalar, upstream_rows, block0, dh_shard,
+                                 ld_shard, lo, shard_rows, dweight_shard, lddw);
+    }
+    // NCCL (or ignore_index): local dH of this shard's vocabulary, then a reduce-scatter
+    char* buf = nullptr;
+    const size_t dh_b = sizeof(float) * static_cast<size_t>(p->n) * p->d;
+    VP_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&buf), dh_b, stream));
+    s = fce_backward(h, p, merged, reduction, upstream_scalar, upstream_rows, reinterpret_cast<float*>(buf), p->d,
+                     dweight_shard, lddw, 0);
+    if (!s) s = fce_sp_scatter(h, c, reinterpret_cast<float*>(buf), p->n, p->d, p->d, dh_shard, shard_rows, ld_shard);
+    cudaFreeAsync(buf, stream);
+    return s;
 }
 
 fce_status fce_dp_step(fce_handle h, fce_comm c, const fce_problem* p, int reduction, float* loss, float* dhidden,

@@ -220,6 +220,27 @@ def native_backward(comm: NativeComm, hidden, weight_shard, targets, v_offset: i
     return dh, dw
 
 
+def native_sp_vp_backward(comm: NativeComm, hidden, weight_shard, targets, v_offset: int, v_total: int,
+                          stats: fce.Stats, shard_rows: int, reduction: str = "mean", upstream=1.0,
+                          ignore_index=None, handle=None):
+    """tp_backward + the sequence-parallel reduce-scatter of dH in one call
+    (fce_sp_vp_backward): -> (this rank's summed dH position shard, local dW
+    shard).  Over a peer-memory transport the reduction runs inside the
+    backward kernel."""
+    import torch
+    h = handle or fce.default_handle(hidden.device.index or 0)
+    p, keep = fce.make_problem(hidden, weight_shard, targets, ignore_index, v_offset, v_total)
+    dev = hidden.device
+    dh = torch.empty(shard_rows, p.d, dtype=torch.float32, device=dev)
+    dw = torch.empty(p.v, p.d, dtype=torch.float32, device=dev)
+    up_rows = None if isinstance(upstream, (int, float)) else upstream.float().contiguous()
+    fce._check(h.lib.fce_sp_vp_backward(h.raw, comm.ptr, ctypes.byref(p), stats.c(), fce.REDUCTIONS[reduction],
+                                        float(upstream) if up_rows is None else 0.0, fce._ptr(up_rows),
+                                        dh.data_ptr() if shard_rows else None, shard_rows, p.d, dw.data_ptr(), p.d),
+               vp=True)
+    return dh, dw
+
+
 def native_sp_gather(comm: NativeComm, hidden_shard, n_total: int, handle=None):
     """sp_to_tp_gather (parallel_sim.hpp:294-314) through fce_sp_gather: this
     rank's position shard of H (bf16) -> the full H on every rank."""

@@ -35,7 +35,13 @@ def main():
     out = vp.native_forward(comm, H, W[lo:hi], Y, lo, v, "mean", ign, handle=h)
     if int(inp["chunks"]):
         h.set_option("vp_overlap_chunks", int(inp["chunks"]))
+    if int(inp["fused"]):
+        h.set_option("vp_fused_dh", 1)
     dh, dw = vp.native_backward(comm, H, W[lo:hi], Y, lo, v, out.stats, "mean", 1.0, ign, handle=h)
+    # sequence-parallel backward: this rank's ceil-first position shard of dH
+    plo, phi = fce.shard_ranges(H.shape[0], k)[rank]
+    dh_sp, _ = vp.native_sp_vp_backward(comm, H, W[lo:hi], Y, lo, v, out.stats, phi - plo, "mean", 1.0, ign,
+                                        handle=h)
     x = torch.from_numpy(inp["x"][rank]).cuda()
     s = vp.native_all_reduce(comm, x.clone(), handle=h)
     g = vp.native_all_gather(comm, torch.full((5,), float(rank), device="cuda"), handle=h)
@@ -43,7 +49,7 @@ def main():
                                   handle=h)
     torch.cuda.synchronize()
     np.savez(sys.argv[5], loss=out.loss.item(), found=out.stats.found.cpu().numpy(), lse=out.lse.cpu().numpy(),
-             dh=dh.cpu().numpy(), dw=dw.cpu().numpy(), s=s.cpu().numpy(), g=g.cpu().numpy(), rs=rs.cpu().numpy())
+             dh=dh.cpu().numpy(), dw=dw.cpu().numpy(), dh_sp=dh_sp.cpu().numpy(), s=s.cpu().numpy(), g=g.cpu().numpy(), rs=rs.cpu().numpy())
     h.close()
     comm.close()
 

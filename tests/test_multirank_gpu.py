@@ -332,8 +332,8 @@ def test_random_multirank_cases(cuda, case):
     assert relmax(np.concatenate([x[2].cpu().numpy() for x in res]), dW) < GRAD_RTOL
 
 
-@pytest.mark.parametrize("k,ign,chunks", [(2, None, 0), (3, -100, 0), (4, None, 2)])
-def test_ipc_transport_multiprocess(cuda, tmp_path, k, ign, chunks):
+@pytest.mark.parametrize("k,ign,chunks,fused", [(2, None, 0, 0), (3, -100, 0, 0), (4, None, 2, 0), (3, None, 0, 1)])
+def test_ipc_transport_multiprocess(cuda, tmp_path, k, ign, chunks, fused):
     """k separate processes (all on this GPU) over the IPC transport: CUDA IPC
     mappings of each rank's registered buffer, cross-process events and a
     shared-memory barrier — the one-process-per-rank data path without NCCL.
@@ -346,7 +346,7 @@ def test_ipc_transport_multiprocess(cuda, tmp_path, k, ign, chunks):
     rng = np.random.default_rng(k)
     x = rng.standard_normal((k, 777)).astype(np.float32)
     inp = tmp_path / "in.npz"
-    np.savez(inp, H=H, W=W, Y=Y, ign=-100, has_ign=int(ign is not None), x=x, chunks=chunks)
+    np.savez(inp, H=H, W=W, Y=Y, ign=-100, has_ign=int(ign is not None), x=x, chunks=chunks, fused=fused)
     uid = vp.NativeComm.ipc_id().hex()
     helper = os.path.join(os.path.dirname(os.path.abspath(__file__)), "helpers", "ipc_rank.py")
     env = dict(os.environ, FCE_LOCAL_TIMEOUT_S="300")
@@ -367,8 +367,68 @@ def test_ipc_transport_multiprocess(cuda, tmp_path, k, ign, chunks):
         np.testing.assert_array_equal(o["found"], st["found"])
         assert abs(float(o["loss"]) - lred) <= LOSS_RTOL * max(1.0, abs(lred))
         assert relmax(o["dh"], dH) < GRAD_RTOL
-        np.testing.assert_array_equal(o["dh"], outs[0]["dh"])
+        if not fused:  # in-kernel peer reduction adds in arrival order
+            np.testing.assert_array_equal(o["dh"], outs[0]["dh"])
         np.testing.assert_array_equal(o["s"], ref_s)
         np.testing.assert_array_equal(o["g"], np.repeat(np.arange(k, dtype=np.float32)[:, None], 5, 1))
         np.testing.assert_array_equal(o["rs"], np.arange(r * 9, r * 9 + 9, dtype=np.float32) * tot)
     assert relmax(np.concatenate([o["dw"] for o in outs]), dW) < GRAD_RTOL
+    assert relmax(np.concatenate([o["dh_sp"] for o in outs]), dH) < GRAD_RTOL  # SP shards, fused reduce-scatter
+
+
+@pytest.mark.parametrize("k,red", [(2, "mean"), (3, "sum"), (8, "none")])
+def test_fused_dh_reduction_in_kernel(cuda, k, red):
+    """Option vp_fused_dh: every rank's dH tiles are TMA-reduce-added straight
+    into the owning rank's accumulator (peer memory) inside the backward; the
+    full dH on every rank equals the oracle."""
+    n, d, v = 700, 136, 2000
+    H, W, Y = ob.make_instance(n, d, v, 300 + k)
+    up = np.linspace(0.5, 1.5, n).astype(np.float32) if red == "none" else 1.0
+    Hd, Wd, Yd = bf16(H), bf16(W), torch.from_numpy(Y).cuda()
+    upd = torch.from_numpy(up).cuda() if red == "none" else 1.0
+    ranges = fce.shard_ranges(v, k)
+
+    def rank_fn(r, comm, h):
+        lo, hi = ranges[r]
+        out = vp.native_forward(comm, Hd, Wd[lo:hi], Yd, lo, v, red, None, handle=h)
+        h.set_option("vp_fused_dh", 1)
+        return vp.native_backward(comm, Hd, Wd[lo:hi], Yd, lo, v, out.stats, red, upd, None, handle=h)
+
+    res = vp.run_ranks(k, rank_fn)
+    st, _, _ = ob.forward(H, W, Y, red)
+    dH, dW = ob.backward(H, W, Y, st, red, up)
+    for dh, _ in res:
+        assert relmax(dh.cpu().numpy(), dH) < GRAD_RTOL
+    assert relmax(np.concatenate([x[1].cpu().numpy() for x in res]), dW) < GRAD_RTOL
+
+
+@pytest.mark.parametrize("k,sizes,ign", [(3, None, None), (4, [70, 0, 500, 130], None), (2, [333, 367], -100)])
+def test_sp_vp_backward_reduce_scatter(cuda, k, sizes, ign):
+    """fce_sp_vp_backward: rank r gets the summed dH rows of its position shard
+    (ragged, unaligned and empty shards; fused in the kernel without ignore,
+    local dH + reduce-scatter with it) and its dW shard."""
+    n, d, v = 700, 72, 1500
+    H, W, Y = ob.make_instance(n, d, v, 410 + k, -100, 0.2 if ign is not None else 0.0)
+    Hd, Wd, Yd = bf16(H), bf16(W), torch.from_numpy(Y).cuda()
+    vr = fce.shard_ranges(v, k)
+    if sizes is None:
+        pr = fce.shard_ranges(n, k)
+    else:
+        e = np.concatenate([[0], np.cumsum(sizes)])
+        pr = [(int(e[i]), int(e[i + 1])) for i in range(k)]
+
+    def rank_fn(r, comm, h):
+        lo, hi = vr[r]
+        out = vp.native_forward(comm, Hd, Wd[lo:hi], Yd, lo, v, "mean", ign, handle=h)
+        return vp.native_sp_vp_backward(comm, Hd, Wd[lo:hi], Yd, lo, v, out.stats, pr[r][1] - pr[r][0], "mean",
+                                        1.0, ign, handle=h)
+
+    res = vp.run_ranks(k, rank_fn)
+    st, _, _ = ob.forward(H, W, Y, "mean", ign)
+    dH, dW = ob.backward(H, W, Y, st, "mean", 1.0, ign)
+    got = np.concatenate([x[0].cpu().numpy() for x in res])
+    assert got.shape == dH.shape
+    assert relmax(got, dH) < GRAD_RTOL
+    if ign is not None:
+        assert np.all(got[Y == ign] == 0.0)
+    assert relmax(np.concatenate([x[1].cpu().numpy() for x in res]), dW) < GRAD_RTOL
