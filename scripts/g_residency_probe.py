@@ -27,7 +27,7 @@ GEOMS = [(0, 0), (4096, 3072), (8192, 1536), (2048, 6144), (16384, 768)]
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--shape", default="16384,4096,128256")
-    ap.add_argument("--geoms", default="", help="rc:band[:l2_hints],... (0:0 = default plan)")
+    ap.add_argument("--geoms", default="", help="rc:band[:l2_hints[:dh_group]],... (0:0 = default plan)")
     a = ap.parse_args()
     n, d, v = (int(x) for x in a.shape.split(","))
     geoms = [tuple(int(y) for y in g.split(":")) for g in a.geoms.split(",")] if a.geoms else GEOMS
@@ -39,6 +39,8 @@ def main():
         h.set_option("validate", 0)
         if len(g) > 2:
             h.set_option("l2_hints", g[2])
+        if len(g) > 3:
+            h.set_option("dh_group", g[3])
         if rc:
             h.set_option("row_chunk", rc)
         if band:
