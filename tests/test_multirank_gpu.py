@@ -432,3 +432,37 @@ def test_sp_vp_backward_reduce_scatter(cuda, k, sizes, ign):
     if ign is not None:
         assert np.all(got[Y == ign] == 0.0)
     assert relmax(np.concatenate([x[1].cpu().numpy() for x in res]), dW) < GRAD_RTOL
+
+
+def test_sp_vp_backward_fallbacks(cuda):
+    """fce_sp_vp_backward where the in-kernel reduction does not apply: a
+    1-rank NCCL communicator (no peer memory) and a width whose fp32 rows are
+    not 16-byte multiples (d % 4 != 0) on the local transport — local dH, then
+    the reduce-scatter; vp_fused_dh falls back the same way."""
+    n, d, v = 300, 70, 900
+    H, W, Y = ob.make_instance(n, d, v, 77)
+    Hd, Wd, Yd = bf16(H), bf16(W), torch.from_numpy(Y).cuda()
+    st, _, _ = ob.forward(H, W, Y, "mean")
+    dH, dW = ob.backward(H, W, Y, st, "mean", 1.0)
+    comm = vp.NativeComm.create_local(device=0)
+    out = vp.native_forward(comm, Hd, Wd, Yd, 0, v, "mean")
+    dh, dw = vp.native_sp_vp_backward(comm, Hd, Wd, Yd, 0, v, out.stats, n, "mean", 1.0)
+    comm.close()
+    assert relmax(dh.cpu().numpy(), dH) < GRAD_RTOL and relmax(dw.cpu().numpy(), dW) < GRAD_RTOL
+    ranges = fce.shard_ranges(v, 2)
+    pr = fce.shard_ranges(n, 2)
+
+    def rank_fn(r, comm, h):
+        lo, hi = ranges[r]
+        o = vp.native_forward(comm, Hd, Wd[lo:hi], Yd, lo, v, "mean", None, handle=h)
+        h.set_option("vp_fused_dh", 1)
+        full, _ = vp.native_backward(comm, Hd, Wd[lo:hi], Yd, lo, v, o.stats, "mean", 1.0, None, handle=h)
+        shard, dw_r = vp.native_sp_vp_backward(comm, Hd, Wd[lo:hi], Yd, lo, v, o.stats, pr[r][1] - pr[r][0],
+                                               "mean", 1.0, None, handle=h)
+        return full.cpu().numpy(), shard.cpu().numpy(), dw_r.cpu().numpy()
+
+    res = vp.run_ranks(2, rank_fn)
+    for full, _, _ in res:
+        assert relmax(full, dH) < GRAD_RTOL
+    assert relmax(np.concatenate([x[1] for x in res]), dH) < GRAD_RTOL
+    assert relmax(np.concatenate([x[2] for x in res]), dW) < GRAD_RTOL
