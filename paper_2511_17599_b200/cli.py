@@ -7,8 +7,10 @@ semantics: every fused method runs through libfce.so on a B200.
 
 `bench` sweeps the (B*T, V) grid per method and emits the reference's CSV
 schema (bench.cpp:200-211): bt,vocab,hidden,method,precision,latency_s,
-latency_min_s,latency_max_s,aux_peak_bytes,loss — `canonical` is the two-stage
-PyTorch path (cuBLAS lm_head GEMM + cross-entropy, materialises N x V logits).
+latency_min_s,latency_max_s,aux_peak_bytes,loss (`--extended` appends
+tokens_per_s,tflops,pct_peak,peak_hbm_bytes,gpus) — `canonical` is the
+two-stage PyTorch path (bf16 cuBLAS lm_head GEMM + fp32 cross-entropy,
+materialises N x V logits; the paper's Table 2 baseline).
 `verify` checks the fused device path against that two-stage path in fp32 on
 random instances (loss equivalence, gradients, window sweep, shard invariance,
 large-offset stability, k-rank vocab-parallel over the in-process transport
@@ -44,17 +46,32 @@ def _deliver(text: str, output):
     os.replace(tmp, output)
 
 
-def _two_stage(H, W, Y, reduction, ign, grads=False):
+def _two_stage(H, W, Y, reduction, ign, grads=False, bf16=False):
+    """The canonical path: lm_head GEMM (materialises N x V logits) + cross-entropy.
+    fp32 GEMM for verify (a float reference); bench uses the bf16 cuBLAS GEMM with an
+    fp32 cross-entropy, the paper's Table 2 "canonical"."""
     import torch
-    Hf = H.float().requires_grad_(grads)
-    Wf = W.float().requires_grad_(grads)
-    z = Hf @ Wf.t()
+    dt = torch.bfloat16 if bf16 else torch.float32
+    Hf = H.to(dt).detach().requires_grad_(grads)
+    Wf = W.to(dt).detach().requires_grad_(grads)
+    z = (Hf @ Wf.t()).float()
     loss = torch.nn.functional.cross_entropy(z, Y, reduction=reduction,
                                              ignore_index=-100 if ign is None else ign)
     if not grads:
         return loss.detach(), None, None
     (loss.sum() if reduction == "none" else loss).backward()
     return loss.detach(), Hf.grad, Wf.grad
+
+
+def _peak_tflops() -> float:
+    """Measured dense bf16 peak of this pool's B200s (MEASURED_PEAKS.json), else the spec."""
+    import json
+    path = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "MEASURED_PEAKS.json")
+    try:
+        with open(path) as f:
+            return float(json.load(f)["bf16_tflops"])
+    except (OSError, KeyError, ValueError):
+        return 2250.0
 
 
 def cmd_bench(a) -> int:
@@ -68,7 +85,8 @@ def cmd_bench(a) -> int:
                 def run():
                     if method == "canonical":
                         with torch.no_grad() if a.forward_only else torch.enable_grad():
-                            loss, _, _ = _two_stage(H, W, Y, a.reduction, None, grads=not a.forward_only)
+                            loss, _, _ = _two_stage(H, W, Y, a.reduction, None, grads=not a.forward_only,
+                                                    bf16=True)
                         return loss
                     if method == "fused_partial_grad":
                         out, parts = fce.fused_forward_with_partial_grads(H, W, Y, a.reduction)
@@ -98,12 +116,22 @@ def cmd_bench(a) -> int:
                 if method != "canonical":
                     aux = max(aux, h.workspace_bytes()[0] - ws0) + h.workspace_bytes()[1]
                 lv = float(loss.sum().item() if loss.dim() else loss.item())
+                peak_hbm = torch.cuda.max_memory_allocated() + (h.workspace_bytes()[1] if method != "canonical" else 0)
                 rows.append((bt, v, a.hidden, method, "bf16", statistics.median(times), min(times), max(times),
-                             int(aux), lv))
+                             int(aux), lv, int(peak_hbm)))
     if a.format == "csv":
-        text = "bt,vocab,hidden,method,precision,latency_s,latency_min_s,latency_max_s,aux_peak_bytes,loss\n"
-        text += "".join(f"{r[0]},{r[1]},{r[2]},{r[3]},{r[4]},{r[5]:.9f},{r[6]:.9f},{r[7]:.9f},{r[8]},{r[9]:.8f}\n"
-                        for r in rows)
+        text = "bt,vocab,hidden,method,precision,latency_s,latency_min_s,latency_max_s,aux_peak_bytes,loss"
+        text += ",tokens_per_s,tflops,pct_peak,peak_hbm_bytes,gpus\n" if a.extended else "\n"
+        peak = _peak_tflops()
+        for r in rows:
+            text += f"{r[0]},{r[1]},{r[2]},{r[3]},{r[4]},{r[5]:.9f},{r[6]:.9f},{r[7]:.9f},{r[8]},{r[9]:.8f}"
+            if a.extended:
+                # algorithmic flops: 2NDV forward; the fused fwd+bwd recomputes the logits (8NDV),
+                # the canonical fwd+bwd does not (6NDV)
+                mult = 2 if a.forward_only else (6 if r[3] == "canonical" else 8)
+                tf = mult * r[0] * r[2] * r[1] / r[5] / 1e12
+                text += f",{r[0] / r[5]:.1f},{tf:.2f},{tf / peak:.4f},{r[10]},1"
+            text += "\n"
     else:
         text = "| B*T | V | method | latency ms | aux MB | loss |\n|---|---|---|---|---|---|\n"
         text += "".join(f"| {r[0]} | {r[1]} | {r[3]} | {r[5] * 1e3:.3f} | {r[8] / 2**20:.1f} | {r[9]:.6f} |\n"
@@ -236,6 +264,8 @@ def main(argv=None) -> int:
     b.add_argument("--warmup", type=int, default=2)
     b.add_argument("--forward-only", action="store_true")
     b.add_argument("--format", default="csv", choices=["csv", "markdown"])
+    b.add_argument("--extended", action="store_true",
+                   help="append tokens_per_s,tflops,pct_peak,peak_hbm_bytes,gpus to the reference CSV schema")
     b.add_argument("--seed", type=int, default=42)
     b.add_argument("--output")
     v = sub.add_parser("verify")

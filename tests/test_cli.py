@@ -61,3 +61,16 @@ def test_bench_losses_match_the_oracle(cuda, tmp_path):
         H, W, Y = ob.make_instance(int(bt), int(hidden), int(vocab), 7)
         _, _, ref = ob.forward(H, W, Y, "sum")
         assert abs(loss - ref) <= 1e-3 * abs(ref), (method, bt, loss, ref)
+
+
+@pytest.mark.gpu
+def test_bench_extended_columns(cuda, tmp_path):
+    out = tmp_path / "e.csv"
+    r = run("bench", "--bt", "512", "--vocab", "4096", "--hidden", "256", "--repeats", "2", "--warmup", "1",
+            "--methods", "canonical,fused", "--extended", "--output", str(out))
+    assert r.returncode == 0, r.stderr
+    lines = out.read_text().strip().splitlines()
+    assert lines[0].endswith(",tokens_per_s,tflops,pct_peak,peak_hbm_bytes,gpus")
+    for l in lines[1:]:
+        f = l.split(",")
+        assert len(f) == 15 and float(f[10]) > 0 and float(f[11]) > 0 and int(f[13]) > 0 and f[14] == "1"
