@@ -93,6 +93,17 @@ fce_status fce_vp_backward(fce_handle h, fce_comm c, const fce_problem* p, fce_s
 fce_status fce_sp_gather(fce_handle h, fce_comm c, const void* shard, int64_t shard_rows, int64_t ld_shard,
                          int64_t d, int64_t n_total, void* full, int64_t ld_full);
 
+/* The sequence-parallel -> vocab-parallel forward as one call: rank r passes
+ * its position shard of H (bf16 [shard_rows, ld_shard]) and a problem whose
+ * `hidden` / `ldh` name a caller-owned full-size buffer (bf16 [n, ldh]) that
+ * receives the gathered H (the backward needs it); weight / v_offset / v_total
+ * / targets as fce_vp_forward.  The other ranks' rows are all-gathered on the
+ * communicator's stream while K1 runs over this rank's own rows, then K1 runs
+ * over the rest and the stats merge as in fce_vp_forward. */
+fce_status fce_sp_vp_forward(fce_handle h, fce_comm c, const fce_problem* p, const void* shard, int64_t shard_rows,
+                             int64_t ld_shard, int reduction, fce_stats merged, float* lse, float* loss_rows,
+                             float* loss_reduced);
+
 /* The backward's inverse of fce_sp_gather: every rank holds a full-length dH
  * partial (fp32 [n_total, lddh], e.g. its vocab shard's contribution); rank r
  * receives the sum over ranks of rows of its position shard (a reduce-scatter

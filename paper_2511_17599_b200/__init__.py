@@ -86,7 +86,8 @@ EXPORTED_SYMBOLS = [
     "fce_comm_group_create", "fce_comm_group_destroy",
     "fce_comm_init_local", "fce_comm_destroy", "fce_comm_query", "fce_vp_last_error", "fce_comm_scratch_bytes",
     "fce_comm_all_gather", "fce_comm_all_reduce_f32", "fce_comm_reduce_scatter_f32",
-    "fce_vp_forward", "fce_vp_backward", "fce_sp_gather", "fce_sp_scatter", "fce_sp_vp_backward", "fce_dp_step",
+    "fce_vp_forward", "fce_vp_backward", "fce_sp_gather", "fce_sp_scatter", "fce_sp_vp_forward", "fce_sp_vp_backward",
+    "fce_dp_step",
 ]
 
 _lib = None
@@ -142,6 +143,7 @@ def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
         "fce_sp_scatter": (I32, [P, P, P, I64, I64, I64, P, I64, I64]),
         "fce_dp_step": (I32, [P, P, ctypes.POINTER(FceProblem), I32, P, P, I64, P, I64]),
         "fce_sp_vp_backward": (I32, [P, P, ctypes.POINTER(FceProblem), FceStats, I32, F, P, P, I64, I64, P, I64]),
+        "fce_sp_vp_forward": (I32, [P, P, ctypes.POINTER(FceProblem), P, I64, I64, I32, FceStats, P, P, P]),
         "fce_vp_last_error": (ctypes.c_char_p, []),
         "fce_vp_forward": (I32, [P, P, ctypes.POINTER(FceProblem), I32, FceStats, P, P, P]),
         "fce_vp_backward": (I32, [P, P, ctypes.POINTER(FceProblem), FceStats, I32, F, P, P, I64, P, I64]),

@@ -123,10 +123,9 @@ fce_status copy_rows(void* dst, size_t ld_dst_bytes, const void* src, size_t ld_
 // then waits on the device counter that marks each chunk's dH rows final; the
 // kernel leaves vp_reserve_sms SMs free so the collective's kernels run beside
 // it.  The handle stream resumes after the last collective.
-fce_status vp_backward_overlapped(fce_handle h, fce_comm c, const fce_problem* p, fce_stats merged, int reduction,
-                                  float upstream_scalar, const float* upstream_rows, float* dhidden,
-                                  float* dweight_shard, int64_t lddw, int64_t chunks) {
-    cudaStream_t stream = fce::handle_stream(h);
+// The communicator's own (high-priority) stream for collectives that overlap
+// the handle stream's kernels, with its two fences.
+fce_status ensure_comm_stream(fce_handle h, fce_comm c) {
     VP_CUDA(cudaSetDevice(fce::handle_device(h)));
     if (!c->comm_stream) {
         int lo = 0, hi = 0;
@@ -135,6 +134,15 @@ fce_status vp_backward_overlapped(fce_handle h, fce_comm c, const fce_problem* p
         VP_CUDA(cudaEventCreateWithFlags(&c->reset_ev, cudaEventDisableTiming));
         VP_CUDA(cudaEventCreateWithFlags(&c->done_ev, cudaEventDisableTiming));
     }
+    return FCE_OK;
+}
+
+fce_status vp_backward_overlapped(fce_handle h, fce_comm c, const fce_problem* p, fce_stats merged, int reduction,
+                                  float upstream_scalar, const float* upstream_rows, float* dhidden,
+                                  float* dweight_shard, int64_t lddw, int64_t chunks) {
+    cudaStream_t stream = fce::handle_stream(h);
+    fce_status es = ensure_comm_stream(h, c);
+    if (es) return es;
     // the comm stream follows everything already queued (inputs of the reduce)
     VP_CUDA(cudaEventRecord(c->done_ev, stream));
     VP_CUDA(cudaStreamWaitEvent(c->comm_stream, c->done_ev, 0));
@@ -430,6 +438,85 @@ fce_status fce_sp_gather(fce_handle h, fce_comm c, const void* shard, int64_t sh
         at += all[4 * q];
     }
     return FCE_OK;
+}
+
+fce_status fce_sp_vp_forward(fce_handle h, fce_comm c, const fce_problem* p, const void* shard, int64_t shard_rows,
+                             int64_t ld_shard, int reduction, fce_stats merged, float* lse, float* loss_rows,
+                             float* loss_reduced) {
+    fce::NvtxRange nvtx_("fce_sp_vp_forward");
+    fce_status s = check_args(h, c);
+    if (s) return s;
+    if (!p || !p->hidden) return vp_fail(FCE_INVALID_ARGUMENT, "null problem or gather buffer");
+    if (p->n <= 0 || p->d <= 0) return vp_fail(FCE_EMPTY_INPUT, "tp forward requires N > 0 and d > 0");
+    if (shard_rows < 0 || (shard_rows > 0 && (!shard || ld_shard < p->d)))
+        return vp_fail(FCE_INVALID_ARGUMENT, "bad hidden shard");
+    const int k = c->impl->nranks, r = c->impl->rank;
+    const int64_t n = p->n, d = p->d;
+    cudaStream_t stream = fce::handle_stream(h);
+    if ((s = ensure_comm_stream(h, c))) return s;
+    // the ranks' position shards
+    std::vector<int64_t> all;
+    const int64_t mine[2] = {shard_rows, d};
+    if ((s = exchange(c, stream, mine, 2, &all))) return s;
+    std::vector<int64_t> start(k + 1, 0);
+    int64_t rows_max = 0;
+    for (int q = 0; q < k; ++q) {
+        if (all[4 * q + 1] != d) return vp_fail(FCE_INVALID_LAYOUT, "hidden shards disagree on width");
+        start[q + 1] = start[q] + all[4 * q];
+        rows_max = std::max(rows_max, all[4 * q]);
+    }
+    if (start[k] != n)
+        return vp_fail(FCE_DIMENSION_MISMATCH, "shard rows add up to %lld, not N = %lld", (long long)start[k],
+                       (long long)n);
+    const int64_t lo = start[r], hi = start[r + 1];
+    // scratch: [packed partials: rank block + k-rank gather] [shard staging + k-rank gather of H shards]
+    const size_t rank_bytes = round_up(13 * static_cast<size_t>(n), 256);
+    const size_t row_b = sizeof(uint16_t) * d;
+    const size_t blk = round_up(row_b * rows_max, 256);
+    char* buf = nullptr;
+    if ((s = scratch(c, rank_bytes * (1 + static_cast<size_t>(k)) + blk * (1 + static_cast<size_t>(k)), stream,
+                     &buf)))
+        return s;
+    char* hbuf = buf + rank_bytes * (1 + static_cast<size_t>(k));
+    char* full = static_cast<char*>(const_cast<void*>(p->hidden));
+    const size_t ldf_b = sizeof(uint16_t) * p->ldh;
+    // 1. this rank's rows into the full H (handle stream), then the other ranks'
+    //    rows arrive on the communicator's stream while K1 runs on these
+    if ((s = copy_rows(full + lo * ldf_b, ldf_b, shard, sizeof(uint16_t) * ld_shard, row_b, shard_rows, stream)))
+        return s;
+    VP_CUDA(cudaEventRecord(c->done_ev, stream));
+    VP_CUDA(cudaStreamWaitEvent(c->comm_stream, c->done_ev, 0));
+    if ((s = copy_rows(hbuf, row_b, shard, sizeof(uint16_t) * ld_shard, row_b, shard_rows, c->comm_stream))) return s;
+    if ((s = c->impl->all_gather(hbuf, hbuf + blk, blk, c->comm_stream))) return s;
+    for (int q = 0; q < k; ++q) {
+        if (q == r) continue;
+        if ((s = copy_rows(full + start[q] * ldf_b, ldf_b, hbuf + blk * (1 + q), row_b, row_b, all[4 * q],
+                           c->comm_stream)))
+            return s;
+    }
+    VP_CUDA(cudaEventRecord(c->reset_ev, c->comm_stream));
+    // 2. K1 over this rank's rows, then (after the gather) over the others
+    float* lm = reinterpret_cast<float*>(buf);
+    uint8_t* lf = reinterpret_cast<uint8_t*>(buf + 12 * n);
+    auto partial = [&](int64_t r0, int64_t r1) -> fce_status {
+        if (r1 <= r0) return FCE_OK;
+        fce_problem q = *p;
+        q.hidden = full + r0 * ldf_b;
+        q.n = r1 - r0;
+        q.targets = p->targets + r0;
+        fce_stats part{lm + r0, lm + n + r0, lm + 2 * n + r0, lf + r0};
+        return fce_forward_partial(h, &q, part);
+    };
+    if ((s = partial(lo, hi))) return s;
+    VP_CUDA(cudaStreamWaitEvent(stream, c->reset_ev, 0));
+    if ((s = partial(0, lo)) || (s = partial(hi, n))) return s;
+    // 3. the packed partials of every rank, merged in rank order (as fce_vp_forward)
+    char* g = buf + rank_bytes;
+    if ((s = c->impl->all_gather(buf, g, rank_bytes, stream))) return s;
+    const float* gm = reinterpret_cast<const float*>(g);
+    return fce::merge_partials(h, k, n, static_cast<int64_t>(rank_bytes / 4), static_cast<int64_t>(rank_bytes), gm,
+                               gm + n, gm + 2 * n, reinterpret_cast<const uint8_t*>(g + 12 * n), p->targets,
+                               p->has_ignore, p->ignore_index, reduction, merged, lse, loss_rows, loss_reduced);
 }
 
 fce_status fce_sp_scatter(fce_handle h, fce_comm c, const float* dh_partial, int64_t n_total, int64_t lddh,

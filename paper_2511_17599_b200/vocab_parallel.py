@@ -220,6 +220,29 @@ def native_backward(comm: NativeComm, hidden, weight_shard, targets, v_offset: i
     return dh, dw
 
 
+def native_sp_vp_forward(comm: NativeComm, hidden_shard, n_total: int, weight_shard, targets, v_offset: int,
+                         v_total: int, reduction: str = "mean", ignore_index=None, handle=None):
+    """sp_to_tp_gather + tp_forward in one call (fce_sp_vp_forward): this rank's
+    position shard of H -> (the gathered full H, FusedOutput); the gather of the
+    other ranks' rows overlaps K1 over this rank's rows."""
+    import torch
+    h = handle or fce.default_handle(hidden_shard.device.index or 0)
+    d = weight_shard.shape[1]
+    ld = (d + 7) // 8 * 8
+    full = torch.empty(n_total, ld, dtype=torch.bfloat16, device=hidden_shard.device)[:, :d]
+    x = fce._as_operand(hidden_shard, "hidden") if hidden_shard.shape[0] else hidden_shard
+    p, keep = fce.make_problem(full, weight_shard, targets, ignore_index, v_offset, v_total)
+    dev = hidden_shard.device
+    st = fce.Stats.empty(n_total, dev)
+    lse = torch.empty(n_total, dtype=torch.float32, device=dev)
+    rows = torch.empty(n_total, dtype=torch.float32, device=dev)
+    red = torch.empty((), dtype=torch.float32, device=dev)
+    fce._check(h.lib.fce_sp_vp_forward(h.raw, comm.ptr, ctypes.byref(p), x.data_ptr() if x.shape[0] else None,
+                                       x.shape[0], x.stride(0) if x.shape[0] else d, fce.REDUCTIONS[reduction],
+                                       st.c(), lse.data_ptr(), rows.data_ptr(), red.data_ptr()), vp=True)
+    return full, fce.FusedOutput(rows if reduction == "none" else red, st, lse, rows)
+
+
 def native_sp_vp_backward(comm: NativeComm, hidden, weight_shard, targets, v_offset: int, v_total: int,
                           stats: fce.Stats, shard_rows: int, reduction: str = "mean", upstream=1.0,
                           ignore_index=None, handle=None):

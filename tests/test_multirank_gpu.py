@@ -466,3 +466,39 @@ def test_sp_vp_backward_fallbacks(cuda):
         assert relmax(full, dH) < GRAD_RTOL
     assert relmax(np.concatenate([x[1] for x in res]), dH) < GRAD_RTOL
     assert relmax(np.concatenate([x[2] for x in res]), dW) < GRAD_RTOL
+
+
+@pytest.mark.parametrize("k,sizes,ign", [(3, None, None), (4, [130, 0, 400, 170], -100)])
+def test_sp_vp_forward_then_backward(cuda, k, sizes, ign):
+    """SP -> TP -> SP: fce_sp_vp_forward (H all-gather overlapped with K1 on the
+    rank's own rows) then fce_sp_vp_backward (dH reduce-scatter in the kernel);
+    every rank's gathered H is bit-exact, stats / loss / dH shards / dW shards
+    match the oracle."""
+    n, d, v = 700, 136, 1800
+    H, W, Y = ob.make_instance(n, d, v, 520 + k, -100, 0.25 if ign is not None else 0.0)
+    Hd, Wd, Yd = bf16(H), bf16(W), torch.from_numpy(Y).cuda()
+    vr = fce.shard_ranges(v, k)
+    if sizes is None:
+        pr = fce.shard_ranges(n, k)
+    else:
+        e = np.concatenate([[0], np.cumsum(sizes)])
+        pr = [(int(e[i]), int(e[i + 1])) for i in range(k)]
+
+    def rank_fn(r, comm, h):
+        lo, hi = vr[r]
+        full, out = vp.native_sp_vp_forward(comm, Hd[pr[r][0]:pr[r][1]], n, Wd[lo:hi], Yd, lo, v, "mean", ign,
+                                            handle=h)
+        dh, dw = vp.native_sp_vp_backward(comm, full, Wd[lo:hi], Yd, lo, v, out.stats, pr[r][1] - pr[r][0],
+                                          "mean", 1.0, ign, handle=h)
+        return full.float().cpu().numpy(), out.loss.item(), out.stats.found.cpu().numpy(), dh.cpu().numpy(), \
+            dw.cpu().numpy()
+
+    res = vp.run_ranks(k, rank_fn)
+    st, _, lred = ob.forward(H, W, Y, "mean", ign)
+    dH, dW = ob.backward(H, W, Y, st, "mean", 1.0, ign)
+    for full, loss, found, _, _ in res:
+        np.testing.assert_array_equal(full, H)
+        np.testing.assert_array_equal(found, st["found"])
+        assert abs(loss - lred) <= LOSS_RTOL * max(1.0, abs(lred))
+    assert relmax(np.concatenate([x[3] for x in res]), dH) < GRAD_RTOL
+    assert relmax(np.concatenate([x[4] for x in res]), dW) < GRAD_RTOL
