@@ -112,6 +112,7 @@ int64_t handle_vp_overlap_chunks(fce_handle h) { return h ? h->vp_overlap_chunks
 int64_t handle_vp_reserve_sms(fce_handle h) { return h ? h->vp_reserve_sms : 0; }
 int handle_device(fce_handle h) { return h ? h->device : 0; }
 int64_t handle_vp_fused_dh(fce_handle h) { return h ? h->vp_fused_dh : 0; }
+bool handle_validate(fce_handle h) { return h && h->validate != 0; }
 unsigned long long* handle_comm_trace(fce_handle h) {
     return h ? reinterpret_cast<unsigned long long*>(h->comm_trace_ptr) : nullptr;
 }

@@ -182,6 +182,8 @@ int64_t handle_vp_overlap_chunks(fce_handle h);
 int64_t handle_vp_reserve_sms(fce_handle h);
 // Option "vp_fused_dh": fce_vp_backward reduces dH inside the kernel (peer memory).
 int64_t handle_vp_fused_dh(fce_handle h);
+// Option "validate" (multi-rank entry points also cross-check the ranks' shapes).
+bool handle_validate(fce_handle h);
 // Option "comm_trace_ptr" (dev): u64 slots for globaltimer stamps, 2 per chunk.
 unsigned long long* handle_comm_trace(fce_handle h);
 cudaError_t launch_stamp(cudaStream_t s, unsigned long long* slot);

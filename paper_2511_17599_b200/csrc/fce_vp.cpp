@@ -16,6 +16,7 @@
 //   fce_dp_step     : dp_step (parallel_sim.hpp:334-378): local fused step,
 //                     all-reduce of loss and dW, scaled by 1 / nranks.
 #include <algorithm>
+#include <climits>
 #include <cstdarg>
 #include <cstdio>
 #include <cstring>
@@ -104,6 +105,26 @@ fce_status exchange(fce_comm c, cudaStream_t s, const int64_t* vals, int cnt, st
 
 fce_status check_args(fce_handle h, fce_comm c) {
     if (!h || !c || !c->impl) return vp_fail(FCE_INVALID_ARGUMENT, "null handle or communicator");
+    return FCE_OK;
+}
+
+// With validation on, the ranks agree on (N, d, V_total, ignore sentinel)
+// before any size-dependent collective: a mismatch is an error on every rank
+// instead of a hang in the collective.
+fce_status check_same_problem(fce_handle h, fce_comm c, const fce_problem* p) {
+    if (!fce::handle_validate(h) || c->impl->nranks == 1) return FCE_OK;
+    std::vector<int64_t> all;
+    const int64_t vt = p->v_total ? p->v_total : p->v;
+    const int64_t mine[4] = {p->n, p->d, vt, p->has_ignore ? p->ignore_index : INT64_MIN};
+    fce_status s = exchange(c, fce::handle_stream(h), mine, 4, &all);
+    if (s) return s;
+    for (int q = 0; q < c->impl->nranks; ++q)
+        for (int i = 0; i < 4; ++i)
+            if (all[4 * q + i] != mine[i])
+                return vp_fail(FCE_DIMENSION_MISMATCH,
+                               "ranks disagree on the problem (N, d, V_total, ignore): rank %d has %lld where this "
+                               "rank has %lld (field %d)",
+                               q, (long long)all[4 * q + i], (long long)mine[i], i);
     return FCE_OK;
 }
 
@@ -342,6 +363,7 @@ fce_status fce_vp_forward(fce_handle h, fce_comm c, const fce_problem* p, int re
     if (s) return s;
     if (!p) return vp_fail(FCE_INVALID_ARGUMENT, "null problem");
     if (p->n <= 0) return vp_fail(FCE_EMPTY_INPUT, "tp forward requires N > 0 and d > 0");
+    if ((s = check_same_problem(h, c, p))) return s;
     const int k = c->impl->nranks;
     const int64_t n = p->n;
     cudaStream_t stream = fce::handle_stream(h);
@@ -370,6 +392,7 @@ fce_status fce_vp_backward(fce_handle h, fce_comm c, const fce_problem* p, fce_s
     if (!dhidden)
         return fce_backward(h, p, merged, reduction, upstream_scalar, upstream_rows, nullptr, 0, dweight_shard,
                             lddw, 0);
+    if ((s = check_same_problem(h, c, p))) return s;
     if (lddh < p->d) return vp_fail(FCE_DIMENSION_MISMATCH, "lddh < d");
     cudaStream_t stream = fce::handle_stream(h);
     if (fce::handle_vp_fused_dh(h) && fused_dh_possible(c, p)) {

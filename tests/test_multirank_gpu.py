@@ -502,3 +502,24 @@ def test_sp_vp_forward_then_backward(cuda, k, sizes, ign):
         assert abs(loss - lred) <= LOSS_RTOL * max(1.0, abs(lred))
     assert relmax(np.concatenate([x[3] for x in res]), dH) < GRAD_RTOL
     assert relmax(np.concatenate([x[4] for x in res]), dW) < GRAD_RTOL
+
+
+def test_ranks_with_different_problems_fail_instead_of_hanging(cuda):
+    """With validation on, fce_vp_forward cross-checks (N, d, V_total, ignore)
+    across the ranks before any size-dependent collective."""
+    d, v = 72, 600
+    W = bf16(ob.make_instance(4, d, v, 1)[1])
+    ranges = fce.shard_ranges(v, 2)
+    got = []
+
+    def rank_fn(r, comm, h):
+        n = 64 + 32 * r
+        H, _, Y = ob.make_instance(n, d, v, r)
+        lo, hi = ranges[r]
+        try:
+            vp.native_forward(comm, bf16(H), W[lo:hi], torch.from_numpy(Y).cuda(), lo, v, "mean", handle=h)
+        except fce.DimensionMismatch:
+            got.append(r)
+
+    vp.run_ranks(2, rank_fn)
+    assert sorted(got) == [0, 1]
