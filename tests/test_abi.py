@@ -112,3 +112,24 @@ int main(void) {
     assert name == "DimensionMismatch"
     import torch
     assert int(code) == (0 if torch.cuda.is_available() else 100)
+
+
+def test_ipc_rendezvous_ids_are_unique_names():
+    """fce_comm_ipc_id needs no GPU: a POSIX shared-memory name, unique per call."""
+    from paper_2511_17599_b200 import vocab_parallel as vp
+    a, b = vp.NativeComm.ipc_id(), vp.NativeComm.ipc_id()
+    na, nb = a.split(b"\0")[0].decode(), b.split(b"\0")[0].decode()
+    assert na.startswith("/fce_ipc_") and nb.startswith("/fce_ipc_") and na != nb
+    assert len(a) == 128
+
+
+def test_comm_entry_points_reject_null_handles():
+    lib = fce.load_library()
+    assert lib.fce_vp_forward(None, None, None, 0, fce.FceStats(), None, None, None) == 102
+    assert lib.fce_sp_vp_backward(None, None, None, fce.FceStats(), 0, 1.0, None, None, 0, 0, None, 0) == 102
+    assert lib.fce_dp_step(None, None, None, 0, None, None, 0, None, 0) == 102
+    g = ctypes.c_void_p()
+    assert lib.fce_comm_group_create(ctypes.byref(g), 0) == 8      # FCE_INVALID_LAYOUT
+    assert lib.fce_comm_group_create(ctypes.byref(g), 65) == 8
+    assert lib.fce_comm_group_create(ctypes.byref(g), 2) == 0
+    assert lib.fce_comm_group_destroy(g) == 0
