@@ -31,7 +31,7 @@ struct fce_comm_s {
     fce::Comm* impl = nullptr;
     void* buf = nullptr;       // grow-only scratch (pack / gather buffers)
     size_t buf_size = 0;
-    int64_t* xchg = nullptr;   // small exchange area: [4] send + [4 * nranks] recv
+    int64_t* xchg = nullptr;   // small exchange area: [8] send + [8 * nranks] recv
     int64_t* xchg_host = nullptr;
     // overlapped backward: the collectives' stream and its two fences
     cudaStream_t comm_stream = nullptr;
@@ -81,26 +81,37 @@ fce_status scratch(fce_comm c, size_t bytes, cudaStream_t s, char** out) {
     return FCE_OK;
 }
 
+constexpr int kXchg = 8;  // int64 values per rank in exchange()
+
 fce_status finish_comm_init(fce_comm c) {
-    const size_t bytes = sizeof(int64_t) * 4 * (1 + static_cast<size_t>(c->impl->nranks));
+    const size_t bytes = sizeof(int64_t) * kXchg * (1 + static_cast<size_t>(c->impl->nranks));
     VP_CUDA(cudaMalloc(&c->xchg, bytes));
     VP_CUDA(cudaMallocHost(&c->xchg_host, bytes));
     return FCE_OK;
 }
 
-// All-gather of up to 4 int64 per rank through the device (host sync):
-// out[r * 4 + i] = rank r's vals[i].
+// All-gather of up to kXchg int64 per rank through the device (host sync):
+// out[r * 4 + i] = rank r's vals[i] for i < 4, and (8-value calls)
+// out[4 * k + r * 4 + i - 4] for i >= 4 — callers index with xval().
 fce_status exchange(fce_comm c, cudaStream_t s, const int64_t* vals, int cnt, std::vector<int64_t>* out) {
     const int k = c->impl->nranks;
     int64_t* host = c->xchg_host;
-    for (int i = 0; i < 4; ++i) host[i] = i < cnt ? vals[i] : 0;
-    VP_CUDA(cudaMemcpyAsync(c->xchg, host, 4 * sizeof(int64_t), cudaMemcpyHostToDevice, s));
-    fce_status st = c->impl->all_gather(c->xchg, c->xchg + 4, 4 * sizeof(int64_t), s);
+    for (int i = 0; i < kXchg; ++i) host[i] = i < cnt ? vals[i] : 0;
+    VP_CUDA(cudaMemcpyAsync(c->xchg, host, kXchg * sizeof(int64_t), cudaMemcpyHostToDevice, s));
+    fce_status st = c->impl->all_gather(c->xchg, c->xchg + kXchg, kXchg * sizeof(int64_t), s);
     if (st) return st;
-    VP_CUDA(cudaMemcpyAsync(host + 4, c->xchg + 4, 4 * sizeof(int64_t) * k, cudaMemcpyDeviceToHost, s));
+    VP_CUDA(cudaMemcpyAsync(host + kXchg, c->xchg + kXchg, kXchg * sizeof(int64_t) * k, cudaMemcpyDeviceToHost, s));
     VP_CUDA(cudaStreamSynchronize(s));
-    out->assign(host + 4, host + 4 + 4 * k);
+    // keep the 4-per-rank layout the callers index (r * 4 + i), then the upper halves
+    out->assign(static_cast<size_t>(kXchg) * k, 0);
+    for (int q = 0; q < k; ++q)
+        for (int i = 0; i < kXchg; ++i)
+            (*out)[i < 4 ? q * 4 + i : 4 * k + q * 4 + (i - 4)] = host[kXchg + q * kXchg + i];
     return FCE_OK;
+}
+
+int64_t xval(const std::vector<int64_t>& all, int k, int q, int i) {
+    return i < 4 ? all[q * 4 + i] : all[4 * k + q * 4 + (i - 4)];
 }
 
 fce_status check_args(fce_handle h, fce_comm c) {
@@ -111,20 +122,24 @@ fce_status check_args(fce_handle h, fce_comm c) {
 // With validation on, the ranks agree on (N, d, V_total, ignore sentinel)
 // before any size-dependent collective: a mismatch is an error on every rank
 // instead of a hang in the collective.
+// (the backward modes — in-kernel peer reduction, overlapped chunks — decide
+// which collectives run, so they must agree too).
 fce_status check_same_problem(fce_handle h, fce_comm c, const fce_problem* p) {
     if (!fce::handle_validate(h) || c->impl->nranks == 1) return FCE_OK;
     std::vector<int64_t> all;
     const int64_t vt = p->v_total ? p->v_total : p->v;
-    const int64_t mine[4] = {p->n, p->d, vt, p->has_ignore ? p->ignore_index : INT64_MIN};
-    fce_status s = exchange(c, fce::handle_stream(h), mine, 4, &all);
+    const int64_t mine[6] = {p->n, p->d, vt, p->has_ignore ? p->ignore_index : INT64_MIN,
+                             fce::handle_vp_fused_dh(h), fce::handle_vp_overlap_chunks(h)};
+    fce_status s = exchange(c, fce::handle_stream(h), mine, 6, &all);
     if (s) return s;
-    for (int q = 0; q < c->impl->nranks; ++q)
-        for (int i = 0; i < 4; ++i)
-            if (all[4 * q + i] != mine[i])
-                return vp_fail(FCE_DIMENSION_MISMATCH,
-                               "ranks disagree on the problem (N, d, V_total, ignore): rank %d has %lld where this "
-                               "rank has %lld (field %d)",
-                               q, (long long)all[4 * q + i], (long long)mine[i], i);
+    const int k = c->impl->nranks;
+    for (int q = 0; q < k; ++q)
+        for (int i = 0; i < 6; ++i)
+            if (xval(all, k, q, i) != mine[i])
+                return vp_fail(i < 4 ? FCE_DIMENSION_MISMATCH : FCE_INVALID_ARGUMENT,
+                               "ranks disagree on the problem / mode (N, d, V_total, ignore, vp_fused_dh, "
+                               "vp_overlap_chunks): rank %d has %lld where this rank has %lld (field %d)",
+                               q, (long long)xval(all, k, q, i), (long long)mine[i], i);
     return FCE_OK;
 }
 

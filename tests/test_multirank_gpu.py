@@ -523,3 +523,23 @@ def test_ranks_with_different_problems_fail_instead_of_hanging(cuda):
 
     vp.run_ranks(2, rank_fn)
     assert sorted(got) == [0, 1]
+
+
+def test_ranks_with_different_backward_modes_fail_instead_of_hanging(cuda):
+    n, d, v = 256, 72, 600
+    H, W, Y = ob.make_instance(n, d, v, 3)
+    Hd, Wd, Yd = bf16(H), bf16(W), torch.from_numpy(Y).cuda()
+    ranges = fce.shard_ranges(v, 2)
+    got = []
+
+    def rank_fn(r, comm, h):
+        lo, hi = ranges[r]
+        out = vp.native_forward(comm, Hd, Wd[lo:hi], Yd, lo, v, "mean", handle=h)
+        h.set_option("vp_fused_dh", r)  # rank 1 asks for the in-kernel reduction, rank 0 does not
+        try:
+            vp.native_backward(comm, Hd, Wd[lo:hi], Yd, lo, v, out.stats, "mean", 1.0, handle=h)
+        except fce.InvalidArgument:
+            got.append(r)
+
+    vp.run_ranks(2, rank_fn)
+    assert sorted(got) == [0, 1]
