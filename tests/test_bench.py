@@ -114,3 +114,14 @@ def test_gpu_arm_ipc_transport_processes(cuda):
                         cwd=ROOT, capture_output=True, text=True, timeout=600)
     d1 = _json_lines(r1.stdout)[0]
     assert abs(d["loss"] - d1["loss"]) <= 1e-5 * abs(d1["loss"])
+
+
+def test_committed_traffic_matches_the_sources():
+    """profiles/traffic.json (ncu --set full DRAM bytes per launch) must have been
+    captured on the current csrc/*: otherwise bench.py would report no traffic."""
+    sys.path.insert(0, ROOT)
+    import bench
+    for cfg in ("llama3-8b", "qwen2.5-7b", "gemma2-2b"):
+        for kernel in ("fce_fwd_sm100", "fce_bwd_persistent_sm100"):
+            t = bench._traffic_from_profile(cfg, kernel)
+            assert t is not None and t["bytes"] > 0, (cfg, kernel)
