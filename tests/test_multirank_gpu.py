@@ -332,7 +332,8 @@ def test_random_multirank_cases(cuda, case):
     assert relmax(np.concatenate([x[2].cpu().numpy() for x in res]), dW) < GRAD_RTOL
 
 
-@pytest.mark.parametrize("k,ign,chunks,fused", [(2, None, 0, 0), (3, -100, 0, 0), (4, None, 2, 0), (3, None, 0, 1)])
+@pytest.mark.parametrize("k,ign,chunks,fused", [(2, None, 0, 0), (3, -100, 0, 0), (4, None, 2, 0), (3, None, 0, 1),
+                                                (8, None, 0, 1)])
 def test_ipc_transport_multiprocess(cuda, tmp_path, k, ign, chunks, fused):
     """k separate processes (all on this GPU) over the IPC transport: CUDA IPC
     mappings of each rank's registered buffer, cross-process events and a
