@@ -60,7 +60,7 @@ struct fce_handle_s {
     int64_t fwd_mc = 0;       // forward on 2-CTA clusters with W multicast
     int64_t bwd_unit_mask = 7;
     int64_t trace_ptr = 0;
-    int64_t bwd_epi_warps = 8;
+    int64_t bwd_epi_warps = 4;  // measured: -1.5 to -2.4% backward, -0.8 to -1.6% step vs 8 (profiles/r02_epi_warps_ab.log)
     int64_t bwd_tma_epi = 3;
     int64_t dh_group = 1;     // bands per dH group in the persistent backward
     int64_t skip_ignored = 1; // compact away ignored rows before the tile kernels

@@ -17,7 +17,7 @@ OPTION_SETS = [
     {"skip_ignored": 0},
     {"row_chunk": 256, "band_cols": 512},
     {"row_chunk": 512, "band_cols": 256, "dh_group": 3},
-    {"bwd_epi_warps": 4},
+    {"bwd_epi_warps": 8},
     {"bwd_tma_epi": 0},
     {"bwd_tma_epi": 1},
     {"bwd_tma_epi": 2},
